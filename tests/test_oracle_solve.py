@@ -1,0 +1,119 @@
+"""Pins for oracle.precond and oracle.pcg (Eq. graphL_precsys, §4).
+
+Fixed by mathematics: pseudo-inverse against numpy's SVD pinv, symmetry and
+positive definiteness of R on the complement of 1, CG on the expanded system
+reproducing CG on the original system iterate by iterate (reading R9), and the
+PCG solution against the dense pseudo-inverse solution.  Fixed by the paper:
+Table 3 / Table 5 iteration counts (bands; the paper's MWM order and FGMRES
+differ from this PCG).
+"""
+import numpy as np
+import pytest
+
+from conftest import read_tables
+from inputs import graphs as G
+from oracle import aggregation as A
+from oracle import expansion as E
+from oracle import graph as GR
+from oracle import pcg as PC
+from oracle import precond as PR
+
+
+def small(seed=0, mu=0.5, side=(6, 5), kind="loguniform"):
+    g = G.grid2d(side[0], side[1], kind, seed)
+    h = A.build_hierarchy(g, seed)
+    return g, h, E.expand(g, h, mu)
+
+
+def test_pinv_solver_against_svd_pinv():
+    g, h, s = small(1)
+    for LX in (s.LT, s.LH):
+        y = np.random.default_rng(0).standard_normal(h.n_tilde)
+        z = PR.PinvSolver(LX)(y)
+        np.testing.assert_allclose(z, np.linalg.pinv(LX.toarray()) @ y, rtol=0,
+                                   atol=1e-10 * np.abs(z).max())
+
+
+@pytest.mark.parametrize("mu", [0.3, 0.8])
+def test_R_against_dense_and_symmetric(mu):
+    g, h, s = small(2, mu)
+    P = s.P()
+    for kind, LX in (("msp", s.LT), ("pegp", s.LH)):
+        R = PR.Preconditioner(P, LX)
+        Rd = PR.dense_R(P, LX)
+        rng = np.random.default_rng(3)
+        for _ in range(3):
+            r = rng.standard_normal(g.n)
+            z = R(r)
+            np.testing.assert_allclose(z, Rd @ r, rtol=0, atol=1e-10 * np.abs(z).max())
+        np.testing.assert_allclose(Rd, Rd.T, rtol=0, atol=1e-10 * np.abs(Rd).max())
+        # positive definite on 1-perp (null(R) in span{1}, R9)
+        Q = np.linalg.qr(np.c_[np.ones(g.n), rng.standard_normal((g.n, g.n - 1))])[0][:, 1:]
+        assert np.linalg.eigvalsh(Q.T @ Rd @ Q).min() > 0
+
+
+def test_expanded_cg_equals_original_pcg():
+    """Reading R9: CG on L_G~ x~ = P^T b preconditioned by L_X^+ produces
+    x_k = P x~_k equal to PCG on L_G x = b with R_X = P L_X^+ P^T."""
+    mu = 0.8
+    g, h, s = small(4, mu, (7, 6))
+    L = GR.laplacian_of_graph(g)
+    P = s.P()
+    b = G.rhs(g.n, 4)
+    inv = PR.PinvSolver(s.LT)
+    R = PR.Preconditioner(P, s.LT)
+    LG = s.LG
+    for k in range(1, 12):
+        xo = PC.pcg(lambda x: L @ x, b, R, 0.0, k).x
+        xt = PC.pcg(lambda x: LG @ x, P.T @ b, inv, 0.0, k).x
+        np.testing.assert_allclose(P @ xt, xo, rtol=0, atol=1e-9 * np.abs(xo).max())
+
+
+@pytest.mark.parametrize("kind", ["msp", "pegp"])
+def test_pcg_solution_against_dense_pinv(kind):
+    g, h, s = small(5, 0.8 if kind == "msp" else 1 / np.sqrt(30), (6, 5), "uniform1_10")
+    L = GR.laplacian_of_graph(g)
+    b = G.rhs(g.n, 5)
+    R = PR.msp(s) if kind == "msp" else PR.pegp(s)
+    res = PC.pcg(lambda x: L @ x, b, R, 1e-10, 500)
+    assert res.converged
+    xs = np.linalg.pinv(L.toarray()) @ b
+    e = res.x - xs
+    e -= e.mean()                      # L-norm is blind to the constant
+    assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs))
+    # residual history ends below tolerance; unpreconditioned CG needs more steps
+    cg = PC.pcg(lambda x: L @ x, b, None, 1e-10, 500)
+    assert res.iterations <= cg.iterations
+
+
+def test_table3_pegp_and_msp_iteration_bands():
+    """PAPER.md Table 3 (l.859-879), unweighted 2D grids, level = max,
+    b = [1,...,1,1-n]^T, tolerance 1e-8: PEGP (mu = 1/sqrt n) 7, 6, 5 steps;
+    MSP 58, 93, 151 steps.  Bands: PEGP within +-2, MSP (mu = 0.8, the
+    paper's practical MSP choice l.1004, reading R11) within 15%."""
+    t = read_tables()
+    for side in (16, 32, 64):
+        n = side * side
+        g = G.grid2d(side, side, "unit")
+        h = A.build_hierarchy(g, 0)
+        L = GR.laplacian_of_graph(g)
+        b = G.rhs_paper(n)
+        s = E.expand(g, h, 1 / np.sqrt(n))
+        it = PC.pcg(lambda x: L @ x, b, PR.pegp(s), 1e-8, 1000).iterations
+        assert abs(it - t["table3_grid_levelmax_pegp_steps"][str(n)]) <= 2, (n, it)
+        s = E.expand_msp_only(g, h, 0.8)
+        it = PC.pcg(lambda x: L @ x, b, PR.msp(s), 1e-8, 1000).iterations
+        assert abs(it / t["table3_grid_levelmax_msp_steps"][str(n)] - 1) <= 0.15, (n, it)
+
+
+def test_table5_watts_strogatz_pegp_band():
+    """PAPER.md Table 5 (l.901-917): Watts-Strogatz, mean degree 4,
+    beta = 1/sqrt n, level = max, mu = 1/sqrt n: PEGP 6, 5 steps (+-2)."""
+    t = read_tables()
+    for n in (256, 1024):
+        g = G.watts_strogatz(n, 4, None, 0)
+        h = A.build_hierarchy(g, 0)
+        L = GR.laplacian_of_graph(g)
+        s = E.expand(g, h, 1 / np.sqrt(n))
+        it = PC.pcg(lambda x: L @ x, G.rhs_paper(n), PR.pegp(s), 1e-8, 1000).iterations
+        assert abs(it - t["table5_ws_levelmax_pegp_steps"][str(n)]) <= 2, (n, it)
