@@ -1,0 +1,716 @@
+// setup.cu -- GPU setup phase of the PEGP/MSP solver (sm_100a).
+//
+// Builds, entirely with device kernels (CUB for sort / scan / run-length):
+//  1. the MWM aggregation hierarchy (§2.2, l.59-70), level by level,
+//     with a parallel "mutual best edge" matching that reproduces the paper's
+//     sequential random-order visit exactly;
+//  2. the Galerkin coarse graphs (the coarse blocks of Eq. def:L_ell);
+//  3. a nested numbering of all levels (every aggregate a contiguous range),
+//     the GPU layout of the expanded vector x~ (n~ = sum n_k entries);
+//  4. the MSP T~ (§3.3) in factored block-tree form: per aggregate the
+//     core-pair 2x2 inverse and per leftover member its elimination
+//     coefficients, subtree sizes, and the dense pseudo-inverse of the top
+//     level -- everything apply_R needs for an exact L_T~^+ solve.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace msp {
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline unsigned grid_for(int64_t n, int tpb = TPB) {
+  int64_t g = (n + tpb - 1) / tpb;
+  return (unsigned)std::max<int64_t>(g, 1);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  // splitmix64 finaliser -- the counter-based generator of reading R1
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------------ MWM
+// Sequential rule: visit vertices in random order; an
+// unmatched vertex takes its heaviest unmatched neighbour (ties: lowest index).
+// Equivalent edge-greedy form: edge {v,u} has key (rank(first), -w, id(second))
+// with first = the endpoint visited first; the sequential rule adds edges in
+// increasing key order when both ends are free.  A round here matches every
+// edge that is the minimum-key free edge of BOTH its endpoints (a local
+// minimum); repeating gives the same matching (lexicographically-first
+// maximal matching).  mate: -1 free, -2 free with no free neighbour, >=0 mate.
+__global__ void k_mwm_propose(int64_t n, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ col, const double* __restrict__ w,
+                              int32_t* __restrict__ mate, int32_t* __restrict__ best,
+                              uint64_t base, unsigned int* __restrict__ nactive) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int found = 0;
+  if (v < n) {
+    int32_t b = -1;
+    if (mate[v] == -1) {
+      const uint64_t pv = mix64(base ^ (uint64_t)v);
+      uint64_t bp = 0;
+      int64_t bf = 0, bs = 0;
+      double bw = 0.0;
+      for (int64_t e = rowptr[v]; e < rowptr[v + 1]; ++e) {
+        const int32_t u = col[e];
+        if (u == v || mate[u] >= 0) continue;
+        const uint64_t pu = mix64(base ^ (uint64_t)u);
+        const bool vfirst = (pv < pu) || (pv == pu && v < u);
+        const uint64_t kp = vfirst ? pv : pu;
+        const int64_t kf = vfirst ? v : (int64_t)u;
+        const int64_t ks = vfirst ? (int64_t)u : v;
+        const double kw = w[e];
+        const bool better =
+            b < 0 || kp < bp ||
+            (kp == bp && (kf < bf || (kf == bf && (kw > bw || (kw == bw && ks < bs)))));
+        if (better) { b = u; bp = kp; bf = kf; bs = ks; bw = kw; }
+      }
+      if (b < 0) mate[v] = -2;  // no free neighbour now or later: a leftover
+    }
+    best[v] = b;
+    found = b >= 0;
+  }
+  unsigned m = __ballot_sync(0xffffffffu, found);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(nactive, (unsigned)__popc(m));
+}
+
+__global__ void k_mwm_match(int64_t n, const int32_t* __restrict__ best, int32_t* __restrict__ mate) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n || mate[v] != -1) return;
+  const int32_t b = best[v];
+  if (b >= 0 && best[b] == (int32_t)v) mate[v] = b;
+}
+
+// pair numbering (reading R3): flag the smaller endpoint of each matched pair
+__global__ void k_pair_flag(int64_t n, const int32_t* __restrict__ mate, int32_t* __restrict__ flag) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < n) flag[v] = (mate[v] > (int32_t)v) ? 1 : 0;
+}
+
+__global__ void k_pair_assign(int64_t n, const int32_t* __restrict__ mate,
+                              const int32_t* __restrict__ scan, int32_t* __restrict__ agg) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t m = mate[v];
+  agg[v] = (m >= 0) ? scan[min((int32_t)v, m)] : -1;
+}
+
+// leftovers join the aggregate of their heaviest neighbour
+__global__ void k_leftover(int64_t n, const int64_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ col, const double* __restrict__ w,
+                           const int32_t* __restrict__ mate, int32_t* __restrict__ agg,
+                           int* __restrict__ err) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n || mate[v] >= 0) return;
+  int32_t b = -1;
+  double bw = 0.0;
+  for (int64_t e = rowptr[v]; e < rowptr[v + 1]; ++e) {
+    const int32_t u = col[e];
+    if (u == v) continue;
+    if (b < 0 || w[e] > bw) { b = u; bw = w[e]; }  // ascending columns: lowest index on ties
+  }
+  if (b < 0) { atomicExch(err, 1); return; }
+  agg[v] = agg[b];  // b is matched (maximality), numbered by k_pair_assign
+}
+
+// --------------------------------------------------------------- coarse graph
+__global__ void k_coarse_count(int64_t n, const int64_t* __restrict__ rowptr,
+                               const int32_t* __restrict__ col, const int32_t* __restrict__ agg,
+                               int64_t* __restrict__ cnt) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int32_t a = agg[u];
+  int64_t c = 0;
+  for (int64_t e = rowptr[u]; e < rowptr[u + 1]; ++e) c += (agg[col[e]] != a);
+  cnt[u] = c;
+}
+
+__global__ void k_coarse_emit(int64_t n, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ col, const int32_t* __restrict__ agg,
+                              const int64_t* __restrict__ pos, int64_t nc,
+                              uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int32_t a = agg[u];
+  int64_t p = pos[u];
+  for (int64_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
+    const int32_t b = agg[col[e]];
+    if (b == a) continue;
+    keys[p] = (uint64_t)a * (uint64_t)nc + (uint64_t)b;
+    vals[p] = e;  // fine entries enumerated in (u, v) order; stable sort keeps it (R4)
+    ++p;
+  }
+}
+
+__global__ void k_coarse_sum(int64_t nruns, const uint64_t* __restrict__ ukeys,
+                             const int64_t* __restrict__ roff, const int64_t* __restrict__ svals,
+                             const double* __restrict__ w, int64_t nc, int32_t* __restrict__ ccol,
+                             double* __restrict__ cw) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nruns) return;
+  double acc = 0.0;
+  for (int64_t j = roff[r]; j < roff[r + 1]; ++j) acc += w[svals[j]];  // left to right (R4)
+  cw[r] = acc;
+  ccol[r] = (int32_t)(ukeys[r] % (uint64_t)nc);
+}
+
+__global__ void k_rowptr_from_keys(int64_t nc, int64_t nruns, const uint64_t* __restrict__ ukeys,
+                                   int64_t* __restrict__ crowptr) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a > nc) return;
+  const uint64_t target = (uint64_t)a * (uint64_t)nc;
+  int64_t lo = 0, hi = nruns;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (ukeys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  crowptr[a] = (a == nc) ? nruns : lo;
+}
+
+// ------------------------------------------------------------ nested order
+__global__ void k_nest_keys(int64_t n, const int32_t* __restrict__ agg, const int32_t* __restrict__ mate,
+                            const int32_t* __restrict__ parent_nested, uint64_t* __restrict__ keys,
+                            int32_t* __restrict__ ids) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t m = mate[v];
+  const uint64_t role = (m >= 0) ? ((int32_t)v < m ? 0u : 1u) : 2u;  // core lo, core hi, leftover
+  keys[v] = (uint64_t)parent_nested[agg[v]] * 3u + role;
+  ids[v] = (int32_t)v;
+}
+
+__global__ void k_scatter_pos(int64_t n, const int32_t* __restrict__ order, int32_t* __restrict__ pos_of) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) pos_of[order[p]] = (int32_t)p;
+}
+
+__global__ void k_cptr(int64_t nparent, int64_t n, const uint64_t* __restrict__ skeys,
+                       int32_t* __restrict__ cptr) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b > nparent) return;
+  if (b == nparent) { cptr[b] = (int32_t)n; return; }
+  const uint64_t target = (uint64_t)b * 3u;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (skeys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  cptr[b] = (int32_t)lo;
+}
+
+__global__ void k_iota32(int64_t n, int32_t* __restrict__ a) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int32_t)i;
+}
+
+// level-1 adjacency in nested numbering (int32 offsets for the solve phase)
+__global__ void k_deg_nested(int64_t n, const int32_t* __restrict__ perm, const int64_t* __restrict__ rowptr,
+                             int32_t* __restrict__ deg) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) { const int32_t v = perm[i]; deg[i] = (int32_t)(rowptr[v + 1] - rowptr[v]); }
+}
+
+__global__ void k_fill_nested(int64_t n, const int32_t* __restrict__ perm, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ col, const double* __restrict__ w,
+                              const int32_t* __restrict__ nested_of, const int32_t* __restrict__ rp1,
+                              int32_t* __restrict__ col1, double* __restrict__ w1) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t v = perm[i];
+  int32_t p = rp1[i];
+  for (int64_t e = rowptr[v]; e < rowptr[v + 1]; ++e, ++p) {
+    col1[p] = nested_of[col[e]];
+    w1[p] = w[e];
+  }
+}
+
+// ------------------------------------------------------------- MSP factors
+// Per level-k node (canonical): parent-edge weight a = mu^{2k-1} * cut, with
+// cut = weight to nodes outside its aggregate (the L_G~ entry of block
+// (k,k+1), Eq. def:L_ell), the matched-edge weight and, for leftovers, the
+// weights to the two core vertices of their aggregate.
+__global__ void k_node_weights(int64_t n, const int64_t* __restrict__ rowptr,
+                               const int32_t* __restrict__ col, const double* __restrict__ w,
+                               const int32_t* __restrict__ agg, const int32_t* __restrict__ mate,
+                               const int32_t* __restrict__ core_lo, const int32_t* __restrict__ core_hi,
+                               double mu_2km1, double* __restrict__ apar, double* __restrict__ wa,
+                               double* __restrict__ wb) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t a = agg[v];
+  const int32_t lo = core_lo[a], hi = core_hi[a];
+  const int32_t m = mate[v];
+  double cut = 0.0, x = 0.0, y = 0.0;
+  for (int64_t e = rowptr[v]; e < rowptr[v + 1]; ++e) {
+    const int32_t u = col[e];
+    if (agg[u] != a) cut += w[e];
+    else if (m >= 0) { if (u == m) x = w[e]; }
+    else { if (u == lo) x = w[e]; else if (u == hi) y = w[e]; }
+  }
+  apar[v] = mu_2km1 * cut;
+  wa[v] = x;  // core: weight to mate;   leftover: weight to core lo
+  wb[v] = y;  // leftover: weight to core hi
+}
+
+__global__ void k_core_ids(int64_t n, const int32_t* __restrict__ mate, const int32_t* __restrict__ agg,
+                           int32_t* __restrict__ core_lo, int32_t* __restrict__ core_hi) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int32_t m = mate[v];
+  if (m > (int32_t)v) { core_lo[agg[v]] = (int32_t)v; core_hi[agg[v]] = m; }
+}
+
+// One thread per aggregate B (nested position at level k+1); its children S
+// are the level-k nested positions [cptr[B], cptr[B+1]): S[0], S[1] the matched
+// pair (u, v), S[2..] leftovers x (each adjacent only to u / v inside S).
+// K_S = sigma L_intra(S) + diag(a_S), sigma = mu^{2(k-1)}.  Eliminating the
+// leftovers into the pair gives  K' = [[q+e_u, -q], [-q, q+e_v]]  with
+//   d_x = a_x + sigma (w_xu + w_xv),  q = sigma w_uv + sum sigma^2 w_xu w_xv / d_x,
+//   e_u = a_u + sum sigma w_xu a_x / d_x,  e_v likewise
+// (all terms positive: no cancellation).  Stored per node (nested index):
+//   S[0]: (Kinv_uu, Kinv_uv, Kinv_vv);  leftover x: (sigma w_xu/d_x, sigma w_xv/d_x, 1/d_x).
+// Also N_B = 1 + sum N_c (subtree sizes in T~) and g_S = K_S^{-1} N_S.
+__global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
+                             const int32_t* __restrict__ order_k,   // nested pos -> canonical (level k)
+                             const double* __restrict__ apar, const double* __restrict__ wa,
+                             const double* __restrict__ wb, double sigma, int64_t off_k,
+                             int64_t off_k1, double* __restrict__ c0, double* __restrict__ c1,
+                             double* __restrict__ c2, double* __restrict__ Nsub,
+                             double* __restrict__ gvec, double* __restrict__ gN_part, int first_level) {
+  int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (B >= nparent) return;
+  const int32_t s0 = cptr[B], s1 = cptr[B + 1];
+  const int32_t cu = order_k[s0], cv = order_k[s0 + 1];
+  const double au = apar[cu], av = apar[cv];
+  const double wuv = wa[cu];
+  double q = sigma * wuv, eu = au, ev = av;
+  for (int32_t p = s0 + 2; p < s1; ++p) {
+    const int32_t x = order_k[p];
+    const double ax = apar[x], wxu = sigma * wa[x], wxv = sigma * wb[x];
+    const double d = ax + wxu + wxv;
+    q += wxu * wxv / d;
+    eu += wxu * ax / d;
+    ev += wxv * ax / d;
+    c0[off_k + p] = wxu / d;
+    c1[off_k + p] = wxv / d;
+    c2[off_k + p] = 1.0 / d;
+  }
+  const double det = q * (eu + ev) + eu * ev;
+  const double kuu = (q + ev) / det, kuv = q / det, kvv = (q + eu) / det;
+  c0[off_k + s0] = kuu; c1[off_k + s0] = kuv; c2[off_k + s0] = kvv;
+  c0[off_k + s0 + 1] = 0.0; c1[off_k + s0 + 1] = 0.0; c2[off_k + s0 + 1] = 0.0;
+  // subtree sizes
+  double NB = 1.0;
+  for (int32_t p = s0; p < s1; ++p) {
+    const double nc = first_level ? 1.0 : Nsub[off_k + p];
+    if (first_level) Nsub[off_k + p] = 1.0;
+    NB += nc;
+  }
+  Nsub[off_k1 + B] = NB;
+  // g_S = K_S^{-1} N_S (same elimination as apply_R)
+  const double Nu = Nsub[off_k + s0], Nv = Nsub[off_k + s0 + 1];
+  double tu = Nu, tv = Nv;
+  for (int32_t p = s0 + 2; p < s1; ++p) {
+    const double t = Nsub[off_k + p];
+    tu += c0[off_k + p] * t;
+    tv += c1[off_k + p] * t;
+  }
+  const double zu = kuu * tu + kuv * tv, zv = kuv * tu + kvv * tv;
+  gvec[off_k + s0] = zu;
+  gvec[off_k + s0 + 1] = zv;
+  double gN = zu * Nu + zv * Nv;
+  for (int32_t p = s0 + 2; p < s1; ++p) {
+    const double t = Nsub[off_k + p];
+    const double zx = c2[off_k + p] * t + c0[off_k + p] * zu + c1[off_k + p] * zv;
+    gvec[off_k + p] = zx;
+    gN += zx * t;
+  }
+  gN_part[B] = gN;
+}
+
+// dense top-level Laplacian sigma_l L_l (top nested order == canonical order)
+__global__ void k_top_dense(int64_t nt, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            const double* __restrict__ w, double sigma, double* __restrict__ M) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  double d = 0.0;
+  for (int64_t j = 0; j < nt; ++j) M[i * nt + j] = 0.0;
+  for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+    M[i * nt + col[e]] = -sigma * w[e];
+    d += sigma * w[e];
+  }
+  M[i * nt + i] = d;
+}
+
+// L^+ = Pi G Pi, G = inverse of the grounded (last node removed) SPD block,
+// Pi = I - 11^T/n.  One block, Gauss-Jordan without pivoting (SPD), nt <= 256.
+__global__ void k_top_pinv(int nt, const double* __restrict__ M, double* __restrict__ A,
+                           double* __restrict__ out) {
+  __shared__ double fac[256];
+  __shared__ double rmean[256];
+  __shared__ double cmean[256];
+  __shared__ double gmean;
+  const int m = nt - 1;
+  const int W = 2 * m;
+  for (int idx = threadIdx.x; idx < m * W; idx += blockDim.x) {  // A = [M_g | I]
+    const int i = idx / W, j = idx % W;
+    A[idx] = (j < m) ? M[i * nt + j] : (j - m == i ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int piv = 0; piv < m; ++piv) {
+    const double inv = 1.0 / A[piv * W + piv];
+    __syncthreads();
+    for (int j = threadIdx.x; j < W; j += blockDim.x) A[piv * W + j] *= inv;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) fac[i] = (i == piv) ? 0.0 : A[i * W + piv];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < m * W; idx += blockDim.x) {
+      const int i = idx / W, j = idx % W;
+      if (i != piv) A[idx] -= fac[i] * A[piv * W + j];
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    double s = 0.0;
+    if (i < m) for (int j = 0; j < m; ++j) s += A[i * W + m + j];
+    rmean[i] = s / nt;
+  }
+  for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+    double s = 0.0;
+    if (j < m) for (int i = 0; i < m; ++i) s += A[i * W + m + j];
+    cmean[j] = s / nt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nt; ++i) s += rmean[i];
+    gmean = s / nt;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nt * nt; idx += blockDim.x) {
+    const int i = idx / nt, j = idx % nt;
+    const double g = (i < m && j < m) ? A[i * W + m + j] : 0.0;
+    out[idx] = g - rmean[i] - cmean[j] + gmean;
+  }
+}
+
+// ------------------------------------------------------------ validation
+__global__ void k_validate(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                           const double* __restrict__ w, int* __restrict__ err) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  int64_t prev = -1;
+  const int64_t e0 = rowptr[v], e1 = rowptr[v + 1];
+  if (e0 == e1) { atomicOr(err, 1); return; }            // isolated vertex
+  for (int64_t e = e0; e < e1; ++e) {
+    const int64_t c = col[e];
+    if (c < 0 || c >= n || c == v || c <= prev) { atomicOr(err, 2); return; }
+    if (!(w[e] > 0.0)) { atomicOr(err, 4); return; }
+    prev = c;
+  }
+}
+
+// ------------------------------------------------------------ CUB helpers
+struct Temp {
+  DBuf<unsigned char> buf;
+  void* get(size_t bytes) {
+    if (bytes > buf.n) buf.alloc(std::max<size_t>(bytes, 1 << 20));
+    return buf.p;
+  }
+};
+
+template <typename T>
+void exclusive_scan(Temp& tmp, const T* in, T* out, int64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  MSP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
+  MSP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes), bytes, in, out, n, st));
+}
+
+template <typename K, typename V>
+void sort_pairs(Temp& tmp, const K* kin, K* kout, const V* vin, V* vout, int64_t n, int end_bit,
+                cudaStream_t st) {
+  size_t bytes = 0;
+  MSP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit, st));
+  MSP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes), bytes, kin, kout, vin, vout, n, 0, end_bit, st));
+}
+
+int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+template <typename T>
+T d2h_scalar(const T* d, cudaStream_t st) {
+  T v;
+  MSP_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+  MSP_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+double reduce_sum(Temp& tmp, const double* in, int64_t n, cudaStream_t st) {
+  DBuf<double> out;
+  out.alloc(1);
+  size_t bytes = 0;
+  MSP_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, in, out.p, n, st));
+  MSP_CUDA(cub::DeviceReduce::Sum(tmp.get(bytes), bytes, in, out.p, n, st));
+  return d2h_scalar(out.p, st);
+}
+
+}  // namespace
+
+void validate_csr(Handle& h, const int64_t* rowptr, const int32_t* col, const double* w, cudaStream_t st) {
+  DBuf<int> err;
+  err.alloc(1);
+  MSP_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
+  k_validate<<<grid_for(h.n), TPB, 0, st>>>(h.n, rowptr, col, w, err.p);
+  MSP_LAUNCH_CHECK();
+  const int e = d2h_scalar(err.p, st);
+  if (e & 1) throw Error{MSP_ERR_GRAPH, "isolated vertex (graph must be connected)"};
+  if (e & 2) throw Error{MSP_ERR_GRAPH, "CSR columns out of range, self loop, or not strictly increasing"};
+  if (e & 4) throw Error{MSP_ERR_GRAPH, "edge weights must be > 0"};
+}
+
+// ------------------------------------------------------------------ driver
+void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const double* w_d,
+                 cudaStream_t st) {
+  Temp tmp;
+  cudaEvent_t e0, e1;
+  MSP_CUDA(cudaEventCreate(&e0));
+  MSP_CUDA(cudaEventCreate(&e1));
+  MSP_CUDA(cudaEventRecord(e0, st));
+
+  const int64_t n = h.n;
+  // ---- level 1 canonical CSR (copy of the input)
+  h.canon_rowptr.emplace_back(); h.canon_rowptr.back().alloc(n + 1);
+  h.canon_col.emplace_back(); h.canon_col.back().alloc(h.nnz_adj);
+  h.canon_w.emplace_back(); h.canon_w.back().alloc(h.nnz_adj);
+  MSP_CUDA(cudaMemcpyAsync(h.canon_rowptr[0].p, rowptr_d, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  MSP_CUDA(cudaMemcpyAsync(h.canon_col[0].p, col_d, h.nnz_adj * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  MSP_CUDA(cudaMemcpyAsync(h.canon_w[0].p, w_d, h.nnz_adj * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  h.lv.clear();
+  h.lv.push_back(LevelHost{n, h.nnz_adj, 0});
+
+  std::vector<DBuf<int32_t>> mates;
+  DBuf<int32_t> best, flag, scan;
+  DBuf<unsigned int> cnt_d;
+  cnt_d.alloc(1);
+  DBuf<int> err_d;
+  err_d.alloc(1);
+  h.mwm_rounds = 0;
+
+  // ---- hierarchy (§2.2; reading R5 for "level = max")
+  for (int k = 1;; ++k) {
+    if (h.levels_req > 0 && (int)h.lv.size() >= h.levels_req) break;
+    const int64_t nk = h.lv.back().n;
+    if (nk <= 2) break;
+    const int64_t* rp = h.canon_rowptr.back().p;
+    const int32_t* cl = h.canon_col.back().p;
+    const double* ww = h.canon_w.back().p;
+    DBuf<int32_t> mate;
+    mate.alloc(nk);
+    best.alloc(nk);
+    MSP_CUDA(cudaMemsetAsync(mate.p, 0xff, nk * sizeof(int32_t), st));  // -1
+    const uint64_t base = mix64(h.seed + 0x9E3779B97F4A7C15ULL * (uint64_t)(k + 1));
+    for (;;) {
+      MSP_CUDA(cudaMemsetAsync(cnt_d.p, 0, sizeof(unsigned), st));
+      k_mwm_propose<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, ww, mate.p, best.p, base, cnt_d.p);
+      MSP_LAUNCH_CHECK();
+      const unsigned active = d2h_scalar(cnt_d.p, st);
+      ++h.mwm_rounds;
+      if (active == 0) break;
+      k_mwm_match<<<grid_for(nk), TPB, 0, st>>>(nk, best.p, mate.p);
+      MSP_LAUNCH_CHECK();
+    }
+    // numbering
+    flag.alloc(nk);
+    scan.alloc(nk);
+    k_pair_flag<<<grid_for(nk), TPB, 0, st>>>(nk, mate.p, flag.p);
+    exclusive_scan(tmp, flag.p, scan.p, nk, st);
+    const int32_t last_scan = d2h_scalar(scan.p + nk - 1, st);
+    const int32_t last_flag = d2h_scalar(flag.p + nk - 1, st);
+    const int64_t nc = (int64_t)last_scan + last_flag;
+    if (nc < 2) break;  // reading R5: keep >= 2 nodes on top
+    DBuf<int32_t> agg;
+    agg.alloc(nk);
+    k_pair_assign<<<grid_for(nk), TPB, 0, st>>>(nk, mate.p, scan.p, agg.p);
+    MSP_CUDA(cudaMemsetAsync(err_d.p, 0, sizeof(int), st));
+    k_leftover<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, ww, mate.p, agg.p, err_d.p);
+    MSP_LAUNCH_CHECK();
+    if (d2h_scalar(err_d.p, st)) throw Error{MSP_ERR_GRAPH, "isolated vertex: graph not connected"};
+
+    // ---- coarse graph (Galerkin weights, reading R4 summation order)
+    DBuf<int64_t> cnt, pos;
+    cnt.alloc(nk + 1);
+    pos.alloc(nk + 1);
+    k_coarse_count<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, agg.p, cnt.p);
+    MSP_CUDA(cudaMemsetAsync(cnt.p + nk, 0, sizeof(int64_t), st));
+    exclusive_scan(tmp, cnt.p, pos.p, nk + 1, st);
+    const int64_t ne = d2h_scalar(pos.p + nk, st);
+    DBuf<uint64_t> keys, skeys, ukeys;
+    DBuf<int64_t> vals, svals, rcnt, roff;
+    keys.alloc(ne); skeys.alloc(ne); vals.alloc(ne); svals.alloc(ne);
+    k_coarse_emit<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, agg.p, pos.p, nc, keys.p, vals.p);
+    MSP_LAUNCH_CHECK();
+    sort_pairs(tmp, keys.p, skeys.p, vals.p, svals.p, ne, bits_for((uint64_t)nc * (uint64_t)nc), st);
+    ukeys.alloc(ne); rcnt.alloc(ne + 1); roff.alloc(ne + 1);
+    DBuf<int64_t> nruns_d;
+    nruns_d.alloc(1);
+    {
+      size_t bytes = 0;
+      MSP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, skeys.p, ukeys.p, rcnt.p, nruns_d.p, ne, st));
+      MSP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(bytes), bytes, skeys.p, ukeys.p, rcnt.p, nruns_d.p, ne, st));
+    }
+    const int64_t nruns = d2h_scalar(nruns_d.p, st);
+    MSP_CUDA(cudaMemsetAsync(rcnt.p + nruns, 0, sizeof(int64_t), st));
+    exclusive_scan(tmp, rcnt.p, roff.p, nruns + 1, st);
+    DBuf<int64_t> crp;
+    DBuf<int32_t> ccol;
+    DBuf<double> cw;
+    crp.alloc(nc + 1); ccol.alloc(nruns); cw.alloc(nruns);
+    k_coarse_sum<<<grid_for(nruns), TPB, 0, st>>>(nruns, ukeys.p, roff.p, svals.p, ww, nc, ccol.p, cw.p);
+    k_rowptr_from_keys<<<grid_for(nc + 1), TPB, 0, st>>>(nc, nruns, ukeys.p, crp.p);
+    MSP_LAUNCH_CHECK();
+
+    mates.push_back(std::move(mate));
+    h.agg_canon.push_back(std::move(agg));
+    h.canon_rowptr.push_back(std::move(crp));
+    h.canon_col.push_back(std::move(ccol));
+    h.canon_w.push_back(std::move(cw));
+    h.lv.push_back(LevelHost{nc, nruns, 0});
+  }
+  h.levels = (int32_t)h.lv.size();
+  const int L = h.levels;
+  int64_t off = 0;
+  for (auto& l : h.lv) { l.off = off; off += l.n; }
+  h.n_tilde = off;
+  const int64_t ntop = h.lv[L - 1].n;
+  if (ntop > h.top_max)
+    throw Error{MSP_ERR_UNSUPPORTED, "top level has " + std::to_string(ntop) +
+                                         " nodes > top_max " + std::to_string(h.top_max)};
+
+  // ---- powers of mu
+  h.neg_mu_pow.assign(2 * L + 2, 1.0);
+  std::vector<double> mu_pow(2 * L + 2, 1.0);
+  for (int j = 1; j < 2 * L + 2; ++j) {
+    mu_pow[j] = mu_pow[j - 1] * h.mu;
+    h.neg_mu_pow[j] = h.neg_mu_pow[j - 1] * (-h.mu);
+  }
+  h.c_sum = 0.0;
+  for (int k = 1; k <= L; ++k) h.c_sum += h.neg_mu_pow[k - 1];
+
+  // ---- nested numbering, top-down
+  h.nested_of_canon.clear();
+  h.nested_of_canon.resize(L);
+  std::vector<DBuf<int32_t>> order(L);  // nested pos -> canonical id
+  h.nested_of_canon[L - 1].alloc(ntop);
+  order[L - 1].alloc(ntop);
+  k_iota32<<<grid_for(ntop), TPB, 0, st>>>(ntop, h.nested_of_canon[L - 1].p);
+  k_iota32<<<grid_for(ntop), TPB, 0, st>>>(ntop, order[L - 1].p);
+  h.cptr_off.assign(L, 0);
+  int64_t cptr_total = 0;
+  for (int k = 1; k < L; ++k) { h.cptr_off[k - 1] = cptr_total; cptr_total += h.lv[k].n + 1; }
+  h.cptr.alloc(std::max<int64_t>(cptr_total, 1));
+  for (int k = L - 1; k >= 1; --k) {
+    const int64_t nk = h.lv[k - 1].n;
+    DBuf<uint64_t> keys, skeys;
+    DBuf<int32_t> ids;
+    keys.alloc(nk); skeys.alloc(nk); ids.alloc(nk);
+    order[k - 1].alloc(nk);
+    h.nested_of_canon[k - 1].alloc(nk);
+    k_nest_keys<<<grid_for(nk), TPB, 0, st>>>(nk, h.agg_canon[k - 1].p, mates[k - 1].p,
+                                              h.nested_of_canon[k].p, keys.p, ids.p);
+    sort_pairs(tmp, keys.p, skeys.p, ids.p, order[k - 1].p, nk, bits_for((uint64_t)h.lv[k].n * 3u), st);
+    k_scatter_pos<<<grid_for(nk), TPB, 0, st>>>(nk, order[k - 1].p, h.nested_of_canon[k - 1].p);
+    k_cptr<<<grid_for(h.lv[k].n + 1), TPB, 0, st>>>(h.lv[k].n, nk, skeys.p, h.cptr.p + h.cptr_off[k - 1]);
+    MSP_LAUNCH_CHECK();
+  }
+
+  // ---- level-1 adjacency in nested numbering
+  if (h.nnz_adj >= (int64_t)INT32_MAX) throw Error{MSP_ERR_UNSUPPORTED, "nnz >= 2^31"};
+  h.perm.alloc(n);
+  MSP_CUDA(cudaMemcpyAsync(h.perm.p, order[0].p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  {
+    DBuf<int32_t> deg;
+    deg.alloc(n + 1);
+    h.rowptr1.alloc(n + 1);
+    k_deg_nested<<<grid_for(n), TPB, 0, st>>>(n, h.perm.p, h.canon_rowptr[0].p, deg.p);
+    MSP_CUDA(cudaMemsetAsync(deg.p + n, 0, sizeof(int32_t), st));
+    exclusive_scan(tmp, deg.p, h.rowptr1.p, n + 1, st);
+    h.col1.alloc(h.nnz_adj);
+    h.w1.alloc(h.nnz_adj);
+    k_fill_nested<<<grid_for(n), TPB, 0, st>>>(n, h.perm.p, h.canon_rowptr[0].p, h.canon_col[0].p,
+                                               h.canon_w[0].p, h.nested_of_canon[0].p, h.rowptr1.p,
+                                               h.col1.p, h.w1.p);
+    MSP_LAUNCH_CHECK();
+  }
+
+  // ---- MSP block-tree factors, bottom-up
+  const int64_t nt = h.n_tilde;
+  h.c0.alloc(nt); h.c1.alloc(nt); h.c2.alloc(nt);
+  h.Nsub.alloc(nt); h.gvec.alloc(nt);
+  MSP_CUDA(cudaMemsetAsync(h.c0.p, 0, nt * sizeof(double), st));
+  MSP_CUDA(cudaMemsetAsync(h.c1.p, 0, nt * sizeof(double), st));
+  MSP_CUDA(cudaMemsetAsync(h.c2.p, 0, nt * sizeof(double), st));
+  MSP_CUDA(cudaMemsetAsync(h.gvec.p, 0, nt * sizeof(double), st));
+  h.apar_canon.clear();
+  h.apar_canon.resize(L > 1 ? L - 1 : 0);
+  double GN = 0.0;
+  for (int k = 1; k < L; ++k) {
+    const int64_t nk = h.lv[k - 1].n, nk1 = h.lv[k].n;
+    DBuf<int32_t> clo, chi;
+    DBuf<double> wa, wb, gpart;
+    clo.alloc(nk1); chi.alloc(nk1);
+    h.apar_canon[k - 1].alloc(nk);
+    wa.alloc(nk); wb.alloc(nk); gpart.alloc(nk1);
+    k_core_ids<<<grid_for(nk), TPB, 0, st>>>(nk, mates[k - 1].p, h.agg_canon[k - 1].p, clo.p, chi.p);
+    k_node_weights<<<grid_for(nk), TPB, 0, st>>>(nk, h.canon_rowptr[k - 1].p, h.canon_col[k - 1].p,
+                                                 h.canon_w[k - 1].p, h.agg_canon[k - 1].p, mates[k - 1].p,
+                                                 clo.p, chi.p, mu_pow[2 * k - 1], h.apar_canon[k - 1].p,
+                                                 wa.p, wb.p);
+    k_msp_factor<<<grid_for(nk1), TPB, 0, st>>>(nk1, h.cptr.p + h.cptr_off[k - 1], order[k - 1].p,
+                                                h.apar_canon[k - 1].p, wa.p, wb.p, mu_pow[2 * (k - 1)],
+                                                h.lv[k - 1].off, h.lv[k].off, h.c0.p, h.c1.p, h.c2.p,
+                                                h.Nsub.p, h.gvec.p, gpart.p, k == 1 ? 1 : 0);
+    MSP_LAUNCH_CHECK();
+    GN += reduce_sum(tmp, gpart.p, nk1, st);
+  }
+  h.GN = GN;
+
+  // ---- top level: dense pseudo-inverse of sigma_l L_l
+  {
+    DBuf<double> M, A;
+    M.alloc(ntop * ntop);
+    A.alloc(std::max<int64_t>((ntop - 1) * 2 * (ntop - 1), 1));
+    h.top_pinv.alloc(ntop * ntop);
+    k_top_dense<<<grid_for(ntop), TPB, 0, st>>>(ntop, h.canon_rowptr[L - 1].p, h.canon_col[L - 1].p,
+                                                h.canon_w[L - 1].p, mu_pow[2 * (L - 1)], M.p);
+    k_top_pinv<<<1, 256, 0, st>>>((int)ntop, M.p, A.p, h.top_pinv.p);
+    MSP_LAUNCH_CHECK();
+    if (L == 1) {  // no hierarchy (n <= 2): N = 1 for all top nodes
+      std::vector<double> ones(ntop, 1.0);
+      MSP_CUDA(cudaMemcpyAsync(h.Nsub.p, ones.data(), ntop * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    MSP_CUDA(cudaStreamSynchronize(st));
+  }
+
+  MSP_CUDA(cudaEventRecord(e1, st));
+  MSP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  MSP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  h.setup_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  h.mates_canon = std::move(mates);
+  h.order_nested = std::move(order);
+}
+
+}  // namespace msp
