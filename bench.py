@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""bench.py -- PCG-MSP solve throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--precond msp] [--mu 0.8] [--rtol 1e-8]
+
+A *step* is one complete PCG solve L_G x = b to rtol 1e-8 (x0 = 0) with the
+MSP preconditioner R = P(mu) L_T~^+ P(mu)^T, on BASELINE configs[1] by default
+(2D 4-neighbour grid 1024x1024, log-uniform[1e-3,1e3] weights, b ~ N(0,1)
+projected off ones).  value = nnz(L_G) x iterations x (ranks) / seconds.
+Setup (GPU hierarchy + expansion + MSP) is timed separately (setup_ms).
+
+Multi-GPU (torchrun, N > 1): each rank solves its own instance of the
+workload (independent problems, no data-path collective) -> "scaling":
+"weak"; timing is the max over ranks.  The row-partitioned single-graph path
+is a §8 "next" row.
+
+--impl reference times the oracle (oracle/, plain fp64 CPU, test
+infrastructure) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG-MSP solve nnz*iters/s"
+UNIT = "nnz*iters/s"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1])); smax.append(float(f[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ byte models
+def spmv_bytes(n: int, nnz_adj: int) -> int:
+    """Algorithmic bytes of one L_G p launch: per row the
+    int32 row offset, p_i read once, q_i written (+ p_i reused for the fused
+    dot); per adjacency entry an int32 column and an fp64 weight."""
+    return n * (4 + 8 + 8) + nnz_adj * (4 + 8)
+
+
+def down1_bytes(n: int, n2: int) -> int:
+    """Level-1 down-sweep: r (8 B) and three fp64 factors (24 B) per node read,
+    z written (8 B); per level-2 node: child pointer (4 B), z_B and w_B (16 B)."""
+    return n * (8 + 24 + 8) + n2 * (4 + 16)
+
+
+def up1_bytes(n: int, n2: int) -> int:
+    """Level-1 up-sweep: r and g read per node (16 B); per level-2 node a
+    child pointer and y_B, s_B written (4 + 16 B)."""
+    return n * 16 + n2 * 20
+
+
+def update_bytes(n: int) -> int:
+    """x += a p ; r -= a q : read x, p, r, q, write x, r."""
+    return n * 48
+
+
+def pupdate_bytes(n: int) -> int:
+    return n * 24
+
+
+# ------------------------------------------------------------ reference arm
+class OracleWorkload:
+    """The oracle (as it stands) on the same workload; setup is untimed."""
+
+    def __init__(self, cfg: int, mu: float, log):
+        from inputs import graphs as G
+        from oracle import aggregation as A, expansion as E, graph as GR, precond as PR
+        t0 = time.time()
+        self.g = G.config_graph(cfg)
+        h = A.build_hierarchy(self.g, 0)
+        self.R = PR.msp(E.expand_msp_only(self.g, h, mu))
+        self.L = GR.laplacian_of_graph(self.g)
+        self.b = G.rhs(self.g.n, 0)
+        log(f"oracle setup {time.time() - t0:.1f}s")
+        self.one = None
+
+    def sample(self, seconds: float):
+        """PCG-MSP iterations for about `seconds`: (nnz*iters/s, iters, secs)."""
+        from oracle import pcg as PC
+        L, R = self.L, self.R
+        if self.one is None:
+            t = time.time()
+            PC.pcg(lambda v: L @ v, self.b, R, 0.0, 1)
+            self.one = max(time.time() - t, 1e-3)
+        iters = max(2, int(seconds / self.one))
+        t = time.time()
+        res = PC.pcg(lambda v: L @ v, self.b, R, 0.0, iters)
+        dt = time.time() - t
+        return self.g.nnz_laplacian * res.iterations / dt, res.iterations, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    log = lambda m: print(f"[bench/reference] {m}", file=sys.stderr, flush=True)
+    wl = OracleWorkload(args.config, args.mu, log)
+    per_step = max(2.0, 90.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v = wl.sample(per_step)
+        if s >= args.warmup:
+            vals.append(v)
+    iters = sum(v[1] for v in vals)
+    secs = sum(v[2] for v in vals)
+    value = wl.g.nnz_laplacian * iters / secs
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / len(vals),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args, wl.g),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{vals[0][1]} PCG-MSP iterations of the oracle per step on the full "
+                                   "graph (scipy SpMV + SuperLU solve of L_T~, one thread; setup untimed)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def config_dict(args, g, extra=None):
+    names = {0: "2D grid 32x32, uniform[1,10] weights", 1: "2D grid 1024x1024, log-uniform[1e-3,1e3] weights",
+             2: "3D 7-point anisotropic grid 256^3", 3: "random geometric graph 4M points",
+             4: "Chung-Lu power-law 50M vertices"}
+    d = {"workload": f"BASELINE configs[{args.config}]: {names.get(args.config, '?')}; PCG+{args.precond.upper()} "
+                     f"to rtol {args.rtol:g}",
+         "n": g.n if g is not None else None, "nnz_L": g.nnz_laplacian if g is not None else None,
+         "precond": args.precond, "mu": args.mu, "rtol": args.rtol, "levels": "max",
+         "parallelism": f"independent problem per rank x{args.gpus}",
+         "l2": "flushed (256 MiB write) before every timed step, inside the timed region"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--precond", default="msp", choices=["msp", "none"])
+    ap.add_argument("--mu", type=float, default=0.8)
+    ap.add_argument("--rtol", type=float, default=1e-8)
+    ap.add_argument("--maxit", type=int, default=200000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    from inputs import graphs as G
+    import paper_2207_07847_b200 as M
+
+    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    g = G.config_graph(args.config, seed=0)
+    b_np = G.rhs(g.n, 0)
+    t0 = time.time()
+    S = M.setup(g.n, torch.as_tensor(g.rowptr, device=dev), torch.as_tensor(g.col, device=dev),
+                torch.as_tensor(g.val, device=dev), mu=args.mu, seed=0)
+    info = S.info()
+    log(f"setup {info['setup_ms']:.1f} ms (wall {time.time() - t0:.1f}s) levels={info['levels']} "
+        f"n~={info['n_tilde']} mwm_rounds={info['mwm_rounds']}")
+    b = torch.as_tensor(b_np, device=dev)
+    x = torch.empty_like(b)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        rep = S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+    log(f"warmup: {rep['iterations']} iterations, converged={rep['converged']}, "
+        f"{rep['solve_ms']:.1f} ms")
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters, launches = [], 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        rep = S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+        iters.append(rep["iterations"])
+        launches += rep["kernel_launches"] + 1
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    it = int(np.median(iters))
+    value = world * g.nnz_laplacian * sum(iters) / (ms_total / 1000.0)
+
+    # ---- e2e: same metric through the C ABI with host buffers (pinned)
+    bh = torch.as_tensor(b_np).pin_memory()
+    xh = torch.empty_like(bh).pin_memory()
+    S.pcg_solve(bh, xh, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+    torch.cuda.synchronize()
+    e_iters = []
+    te = time.perf_counter()
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.fill_(1.0)
+        r2 = S.pcg_solve(bh, xh, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+        e_iters.append(r2["iterations"])
+    torch.cuda.synchronize()
+    te = time.perf_counter() - te
+    e2e_value = world * g.nnz_laplacian * sum(e_iters) / te
+
+    # ---- profiled replay of one step: per-kernel device time (CUDA events)
+    S.set_profiling(True)
+    flush.fill_(1.0)
+    S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+    S.set_profiling(False)
+    prof = S.get_profile()
+    sizes = S.level_sizes()
+    n2 = int(sizes[1]) if len(sizes) > 1 else 0
+    nnz_adj = int(g.rowptr[-1])
+    model = {"spmv": spmv_bytes(g.n, nnz_adj), "down_level1": down1_bytes(g.n, n2),
+             "up_level1": up1_bytes(g.n, n2), "update": update_bytes(g.n), "p_update": pupdate_bytes(g.n)}
+    hbm, peak_src = measured_peaks()
+    breakdown = {}
+    for k, v in prof.items():
+        if v["launches"]:
+            avg = v["ms"] / v["launches"]
+            e = {"total_ms": round(v["ms"], 3), "launches": v["launches"], "avg_us": round(avg * 1000, 3)}
+            if k in model:
+                e["GBps"] = round(model[k] / (avg / 1000) / 1e9, 1)
+            breakdown[k] = e
+    dom = max((k for k in breakdown if k in model), key=lambda k: breakdown[k]["total_ms"])
+    ach = model[dom] / (breakdown[dom]["avg_us"] * 1e-6) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": model[dom]}
+    prof_total = sum(v["ms"] for v in prof.values())
+    solve_bytes = sum(model.get(k, 0) * prof[k]["launches"] for k in prof)
+    whole_gbps = solve_bytes / (prof_total / 1000) / 1e9 if prof_total else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, cit, cdt = OracleWorkload(args.config, args.mu, log).sample(15.0)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": f"{cit} PCG-MSP iterations of the oracle on the full graph in {cdt:.1f}s "
+                             "(scipy SpMV + SuperLU solve of L_T~, single thread; oracle setup untimed)"}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, g, {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"])}),
+            "iterations": it, "time_to_rtol_s": ms_step / 1000.0, "setup_ms": info["setup_ms"],
+            "solve_GBps_algorithmic": round(whole_gbps, 1) if whole_gbps else None,
+            "roofline": roofline, "kernel_breakdown": breakdown,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * g.n,
+                    "d2h_bytes_per_step": 8 * g.n},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

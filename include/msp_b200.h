@@ -148,6 +148,19 @@ int msp_apply_R(msp_handle* h, int precond, const double* r, double* z, int mem,
 int msp_pcg_solve(msp_handle* h, int precond, const double* b, double* x, double rtol,
                   int32_t maxit, int mem, void* stream, msp_report* report);
 
+/*
+ * Kernel-level profiling of msp_pcg_solve (measurement support, DESIGN.md §8
+ * "Measurement").  When enabled, every launch of the solve is bracketed by
+ * CUDA events on the solve's stream and its device time is accumulated per
+ * category: 0 L_G SpMV (+dot), 1 x/r update (+norm), 2 level-1 up-sweep,
+ * 3 coarse up-sweeps, 4 top solve, 5 coarse down-sweeps, 6 level-1
+ * down-sweep (+dot), 7 p update.  msp_get_profile copies ms[MSP_PROF_NCAT]
+ * and launch counts counts[MSP_PROF_NCAT] (host arrays) and resets them.
+ */
+#define MSP_PROF_NCAT 8
+int msp_set_profiling(msp_handle* h, int on);
+int msp_get_profile(msp_handle* h, double* ms, int64_t* counts);
+
 /* Thread-local description of the last error (never NULL). */
 const char* msp_last_error(void);
 

@@ -65,9 +65,12 @@ def _load():
     L.msp_apply_L.argtypes = [P, P, P, ctypes.c_int, P]
     L.msp_apply_R.argtypes = [P, ctypes.c_int, P, P, ctypes.c_int, P]
     L.msp_pcg_solve.argtypes = [P, ctypes.c_int, P, P, d, i32, ctypes.c_int, P, ctypes.POINTER(_Report)]
+    L.msp_set_profiling.argtypes = [P, ctypes.c_int]
+    L.msp_get_profile.argtypes = [P, P, P]
     L.msp_last_error.restype = ctypes.c_char_p
     for f in ("msp_setup", "msp_destroy", "msp_info", "msp_level_sizes", "msp_get_aggregates",
-              "msp_get_msp_edges", "msp_apply_L", "msp_apply_R", "msp_pcg_solve"):
+              "msp_get_msp_edges", "msp_apply_L", "msp_apply_R", "msp_pcg_solve", "msp_set_profiling",
+              "msp_get_profile"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -162,6 +165,19 @@ class Solver:
         _check(_lib.msp_get_msp_edges(self._h, ctypes.byref(cnt), i.ctypes.data, j.ctypes.data,
                                       w.ctypes.data))
         return i, j, w
+
+    PROFILE_CATEGORIES = ("spmv", "update", "up_level1", "up_coarse", "top", "down_coarse",
+                          "down_level1", "p_update")
+
+    def set_profiling(self, on: bool = True):
+        _check(_lib.msp_set_profiling(self._h, 1 if on else 0))
+
+    def get_profile(self) -> dict:
+        ms = np.zeros(8, dtype=np.float64)
+        cnt = np.zeros(8, dtype=np.int64)
+        _check(_lib.msp_get_profile(self._h, ms.ctypes.data, cnt.ctypes.data))
+        return {c: {"ms": float(ms[i]), "launches": int(cnt[i])}
+                for i, c in enumerate(self.PROFILE_CATEGORIES)}
 
     # ---------------------------------------------------------- hot path
     def apply_L(self, x, y=None, stream=None):

@@ -263,4 +263,23 @@ int msp_pcg_solve(msp_handle* H, int precond, const double* b, double* x, double
   });
 }
 
+int msp_set_profiling(msp_handle* H, int on) {
+  return guarded([&] {
+    need(H != nullptr, "null handle");
+    H->h.profile = on ? 1 : 0;
+  });
+}
+
+int msp_get_profile(msp_handle* H, double* ms, int64_t* counts) {
+  return guarded([&] {
+    need(H && ms && counts, "null argument");
+    for (int i = 0; i < MSP_PROF_NCAT; ++i) {
+      ms[i] = H->h.prof_ms[i];
+      counts[i] = H->h.prof_cnt[i];
+      H->h.prof_ms[i] = 0.0;
+      H->h.prof_cnt[i] = 0;
+    }
+  });
+}
+
 }  // extern "C"

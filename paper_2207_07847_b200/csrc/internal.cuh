@@ -12,6 +12,8 @@
 
 namespace msp {
 
+enum { PC_SPMV = 0, PC_UPDATE, PC_UP1, PC_UPC, PC_TOP, PC_DOWNC, PC_DOWN1, PC_PUPD };
+
 // ---------------------------------------------------------------- errors
 struct Error {
   int code;
@@ -111,6 +113,9 @@ struct Handle {
   DBuf<double> stage_in, stage_out;   // host-mode staging
   int64_t red_cap = 0;
   int64_t launches = 0;       // kernels launched (counted on the host)
+  int profile = 0;            // bracket solve launches with events (msp_set_profiling)
+  double prof_ms[MSP_PROF_NCAT] = {0};
+  int64_t prof_cnt[MSP_PROF_NCAT] = {0};
 };
 
 // setup.cu

@@ -411,6 +411,47 @@ void launch_spmv(Handle& h, const double* x, double* y, cudaStream_t st) {
   ++h.launches;
 }
 
+// ----------------------------------------------------------- profiling
+// When h.profile is set, every launch of the solve is bracketed by CUDA
+// events on the launching stream; per-category device time is accumulated
+// (msp_get_profile).  Off by default: the timed bench steps run unbracketed.
+struct Prof {
+  Handle& h;
+  cudaStream_t st;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> cat;
+  explicit Prof(Handle& hh, cudaStream_t s) : h(hh), st(s) {}
+  ~Prof() { flush(); }
+  void begin() {
+    if (!h.profile) return;
+    cudaEvent_t e;
+    MSP_CUDA(cudaEventCreate(&e));
+    MSP_CUDA(cudaEventRecord(e, st));
+    ev.push_back(e);
+  }
+  void end(int c) {
+    if (!h.profile) return;
+    cudaEvent_t e;
+    MSP_CUDA(cudaEventCreate(&e));
+    MSP_CUDA(cudaEventRecord(e, st));
+    ev.push_back(e);
+    cat.push_back(c);
+  }
+  void flush() {
+    if (ev.empty()) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t i = 0; i < cat.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      h.prof_ms[cat[i]] += ms;
+      h.prof_cnt[cat[i]] += 1;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    cat.clear();
+  }
+};
+
 // partial-sum region of the up-sweep of level k (children at level k)
 int64_t up_part_off(const Handle& h, int k) {
   int64_t o = 0;
@@ -419,7 +460,9 @@ int64_t up_part_off(const Handle& h, int k) {
 }
 
 // R r for the MSP, nested numbering; mode 0: plain apply, 1: PCG init, 2: PCG iteration
-void msp_sweeps(Handle& h, const double* r, double* z, cudaStream_t st, int mode) {
+void msp_sweeps(Handle& h, const double* r, double* z, cudaStream_t st, int mode, Prof* pf = nullptr) {
+  Prof local(h, st);
+  Prof& P = pf ? *pf : local;
   const int L = h.levels;
   const int check = mode >= 2 ? 1 : 0;
   double* part = h.red.p;
@@ -435,22 +478,27 @@ void msp_sweeps(Handle& h, const double* r, double* z, cudaStream_t st, int mode
     const LevelHost& lk1 = h.lv[k];
     const double* yin = (k == 1) ? r : h.Y.p + lk.off;
     const double* sin = (k == 1) ? r : h.S.p + lk.off;
+    P.begin();
     k_up<<<grid_for(lk1.n), TPB, 0, st>>>(lk1.n, h.cptr.p + h.cptr_off[k - 1], yin, sin, h.gvec.p + lk.off,
                                           h.Y.p + lk1.off, h.S.p + lk1.off, h.neg_mu_pow[k],
                                           part_up + up_part_off(h, k), h.counters.p, check);
     MSP_LAUNCH_CHECK();
+    P.end(k == 1 ? PC_UP1 : PC_UPC);
     ++h.launches;
   }
   const LevelHost& lt = h.lv[L - 1];
   const int64_t npart = up_part_off(h, L);
+  P.begin();
   k_top<256><<<1, 256, 0, st>>>((int)lt.n, h.Y.p + lt.off, h.S.p + lt.off, h.Nsub.p + lt.off, h.top_pinv.p,
                                 part_up, npart, h.c_sum, (double)h.n_tilde, h.GN, h.Z.p + lt.off,
                                 h.W.p + lt.off, h.scal.p, h.counters.p, check);
   MSP_LAUNCH_CHECK();
+  P.end(PC_TOP);
   ++h.launches;
   for (int k = L - 1; k >= 1; --k) {
     const LevelHost& lk = h.lv[k - 1];
     const LevelHost& lk1 = h.lv[k];
+    P.begin();
     if (k >= 2) {
       k_down<false><<<grid_for(lk1.n), TPB, 0, st>>>(
           lk1.n, h.cptr.p + h.cptr_off[k - 1], h.S.p + lk.off, h.Nsub.p + lk.off, h.c0.p + lk.off,
@@ -462,6 +510,7 @@ void msp_sweeps(Handle& h, const double* r, double* z, cudaStream_t st, int mode
           h.W.p + lk1.off, nullptr, z, -h.mu, part, h.scal.p, h.counters.p, mode);
     }
     MSP_LAUNCH_CHECK();
+    P.end(k == 1 ? PC_DOWN1 : PC_DOWNC);
     ++h.launches;
   }
 }
@@ -534,21 +583,29 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
   MSP_LAUNCH_CHECK();
 
   unsigned host_cnt[C_NCNT];
-  const int check_every = 16;
+  const int check_every = h.profile ? 1 : 16;
+  Prof P(h, st);
   int it = 0;
   while (it < maxit) {
     const int batch = std::min(check_every, maxit - it);
     for (int b2 = 0; b2 < batch; ++b2) {
+      P.begin();
       launch_spmv<true>(h, h.vp.p, h.vq.p, st);                 // q = L p, alpha
+      P.end(PC_SPMV);
+      P.begin();
       k_update<<<gv, TPB, 0, st>>>(n, x, h.vr.p, h.vp.p, h.vq.p, h.red.p, h.scal.p, h.counters.p);
+      P.end(PC_UPDATE);
       ++h.launches;
-      if (precond == MSP_PRECOND_MSP) msp_sweeps(h, h.vr.p, h.vz.p, st, 2);  // z = R r, beta
+      if (precond == MSP_PRECOND_MSP) msp_sweeps(h, h.vr.p, h.vz.p, st, 2, &P);  // z = R r, beta
       else { k_copy_dot<<<gv, TPB, 0, st>>>(n, h.vr.p, h.vz.p, h.red.p, h.scal.p, h.counters.p, 2); ++h.launches; }
+      P.begin();
       k_pupdate<<<gv, TPB, 0, st>>>(n, h.vz.p, h.vp.p, h.scal.p, h.counters.p, 1);
+      P.end(PC_PUPD);
       ++h.launches;
       MSP_LAUNCH_CHECK();
     }
     it += batch;
+    P.flush();
     MSP_CUDA(cudaMemcpyAsync(host_cnt, h.counters.p, sizeof(host_cnt), cudaMemcpyDeviceToHost, st));
     MSP_CUDA(cudaStreamSynchronize(st));
     if (host_cnt[C_DONE]) break;
