@@ -75,7 +75,25 @@ def _load():
     return L
 
 
-_lib = _load()
+class _LazyLib:
+    """Loads libmsp_b200.so on first use and raises ImportError if it is not
+    built (no CPU fallback).  Lazy so that ``paper_2207_07847_b200.build`` can
+    be imported to build it."""
+
+    _L = None
+
+    def __getattr__(self, name):
+        if _LazyLib._L is None:
+            _LazyLib._L = _load()
+        return getattr(_LazyLib._L, name)
+
+
+_lib = _LazyLib()
+
+
+def load():
+    """Force-load the native library (raises ImportError if missing)."""
+    return _lib.msp_last_error and _LazyLib._L
 
 
 def _check(rc: int):
