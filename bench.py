@@ -103,32 +103,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ byte models
+# Algorithmic HBM bytes per launch: every array the
+# kernel must touch, once; gathered neighbour values are L2 re-reads and are
+# not counted.
 def spmv_bytes(n: int, nnz_adj: int) -> int:
-    """Algorithmic bytes of one L_G p launch: per row the
-    int32 row offset, p_i read once, q_i written (+ p_i reused for the fused
-    dot); per adjacency entry an int32 column and an fp64 weight."""
-    return n * (4 + 8 + 8) + nnz_adj * (4 + 8)
+    """p = z + beta p_old fused with q = L_G p and (p, q): per row the int32
+    row offset, z_i and p_old_i read, p_i and q_i written (4 + 4*8 B); per
+    adjacency entry an int32 column and an fp64 weight (12 B)."""
+    return n * 36 + nnz_adj * 12
 
 
-def down1_bytes(n: int, n2: int) -> int:
-    """Level-1 down-sweep: r (8 B) and three fp64 factors (24 B) per node read,
-    z written (8 B); per level-2 node: child pointer (4 B), z_B and w_B (16 B)."""
-    return n * (8 + 24 + 8) + n2 * (4 + 16)
+def tile_up_bytes(sizes, kt: int) -> int:
+    """x += a p, r -= a q (x, p, r, q read, x, r written: 48 B per level-1
+    node); g read for levels 1..Kt (8 B); child pointers of levels 2..Kt
+    (4 B); y written at level Kt (8 B)."""
+    n = sizes[0]
+    return 48 * n + 8 * sum(sizes[:kt]) + 4 * sum(sizes[1:kt]) + 8 * sizes[kt - 1] * (kt > 1)
 
 
-def up1_bytes(n: int, n2: int) -> int:
-    """Level-1 up-sweep: r and g read per node (16 B); per level-2 node a
-    child pointer and y_B, s_B written (4 + 16 B)."""
-    return n * 16 + n2 * 20
-
-
-def update_bytes(n: int) -> int:
-    """x += a p ; r -= a q : read x, p, r, q, write x, r."""
-    return n * 48
-
-
-def pupdate_bytes(n: int) -> int:
-    return n * 24
+def tile_down_bytes(sizes, kt: int) -> int:
+    """r read and R r written (16 B per level-1 node); factors c0, c1, c2 of
+    levels 1..Kt-1 (24 B); subtree sizes N of levels 2..Kt-1 (8 B); child
+    pointers of levels 2..Kt (4 B); z, w read at level Kt (16 B)."""
+    n = sizes[0]
+    return (16 * n + 24 * sum(sizes[:kt - 1]) + 8 * sum(sizes[1:kt - 1]) + 4 * sum(sizes[1:kt])
+            + 16 * sizes[kt - 1])
 
 
 # ------------------------------------------------------------ reference arm
@@ -309,8 +308,11 @@ def main():
     sizes = S.level_sizes()
     n2 = int(sizes[1]) if len(sizes) > 1 else 0
     nnz_adj = int(g.rowptr[-1])
-    model = {"spmv": spmv_bytes(g.n, nnz_adj), "down_level1": down1_bytes(g.n, n2),
-             "up_level1": up1_bytes(g.n, n2), "update": update_bytes(g.n), "p_update": pupdate_bytes(g.n)}
+    sz = [int(v) for v in sizes]
+    kt = int(info["tile_level"])
+    model = {"spmv": spmv_bytes(g.n, nnz_adj), "tile_up": tile_up_bytes(sz, kt)}
+    if kt >= 2:
+        model["tile_down"] = tile_down_bytes(sz, kt)
     hbm, peak_src = measured_peaks()
     breakdown = {}
     for k, v in prof.items():
@@ -351,7 +353,10 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, g, {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"])}),
+            "config": config_dict(args, g, {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"]),
+                                             "tile_level": int(info["tile_level"]),
+                                             "coarse_level": int(info["coarse_level"]),
+                                             "ntiles": int(info["ntiles"]), "ntiers": int(info["ntiers"])}),
             "iterations": it, "time_to_rtol_s": ms_step / 1000.0, "setup_ms": info["setup_ms"],
             "solve_GBps_algorithmic": round(whole_gbps, 1) if whole_gbps else None,
             "roofline": roofline, "kernel_breakdown": breakdown,

@@ -69,6 +69,14 @@ typedef struct msp_info_t {
   int32_t mwm_rounds;   /* parallel matching rounds used over all levels        */
   double mu;            /* mu actually used                                     */
   double setup_ms;      /* GPU setup time (hierarchy + expansion + MSP), device */
+  /* solve schedule: levels 1..coarse_level run
+     as ntiers tiers of tile kernels (the first covers levels 1..tile_level
+     with ntiles CTAs), levels coarse_level..l in one single-CTA kernel */
+  int32_t tile_level;
+  int32_t coarse_level;
+  int64_t ntiles;       /* tiles (CTAs) of the first tier                       */
+  int32_t ntiers;
+  int32_t spmv_grid;    /* CTAs of the L_G product                              */
 } msp_info_t;
 
 typedef struct msp_report {
@@ -149,13 +157,16 @@ int msp_pcg_solve(msp_handle* h, int precond, const double* b, double* x, double
                   int32_t maxit, int mem, void* stream, msp_report* report);
 
 /*
- * Kernel-level profiling of msp_pcg_solve (measurement support, DESIGN.md §8
+ * Kernel-level profiling of msp_pcg_solve (measurement support, DESIGN.md
  * "Measurement").  When enabled, every launch of the solve is bracketed by
- * CUDA events on the solve's stream and its device time is accumulated per
- * category: 0 L_G SpMV (+dot), 1 x/r update (+norm), 2 level-1 up-sweep,
- * 3 coarse up-sweeps, 4 top solve, 5 coarse down-sweeps, 6 level-1
- * down-sweep (+dot), 7 p update.  msp_get_profile copies ms[MSP_PROF_NCAT]
- * and launch counts counts[MSP_PROF_NCAT] (host arrays) and resets them.
+ * CUDA events on the solve's stream (the iterations then run without the
+ * captured CUDA graph) and its device time is accumulated per category:
+ * 0 p = z + beta p fused with q = L_G p and (p, q);  1 tile up-sweep fused
+ * with x/r update and (r, r);  2 per-level up-sweeps;  3 single-CTA coarse
+ * kernel (coarse up-sweep, top solve, coarse down-sweep);  4 per-level
+ * down-sweeps;  5 tile down-sweep with the output R r and (r, R r);  6, 7
+ * unused.  msp_get_profile copies ms[MSP_PROF_NCAT] and launch counts
+ * counts[MSP_PROF_NCAT] (host arrays) and resets them.
  */
 #define MSP_PROF_NCAT 8
 int msp_set_profiling(msp_handle* h, int on);

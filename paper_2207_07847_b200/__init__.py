@@ -12,7 +12,7 @@ box without the built library raises.
 """
 from ._lib import (  # noqa: F401
     MSP_MEM_DEVICE, MSP_MEM_HOST, MSP_PRECOND_MSP, MSP_PRECOND_NONE, MSP_PRECOND_PEGP,
-    MspError, Solver, library_path, setup,
+    MspError, Solver, library_path, load, setup,
 )
 
 __all__ = ["setup", "Solver", "MspError", "library_path", "MSP_PRECOND_MSP", "MSP_PRECOND_PEGP",

@@ -37,7 +37,9 @@ class _Params(ctypes.Structure):
 class _Info(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("n_tilde", ctypes.c_int64),
                 ("levels", ctypes.c_int32), ("mwm_rounds", ctypes.c_int32), ("mu", ctypes.c_double),
-                ("setup_ms", ctypes.c_double)]
+                ("setup_ms", ctypes.c_double), ("tile_level", ctypes.c_int32),
+                ("coarse_level", ctypes.c_int32), ("ntiles", ctypes.c_int64),
+                ("ntiers", ctypes.c_int32), ("spmv_grid", ctypes.c_int32)]
 
 
 class _Report(ctypes.Structure):
@@ -184,8 +186,8 @@ class Solver:
                                       w.ctypes.data))
         return i, j, w
 
-    PROFILE_CATEGORIES = ("spmv", "update", "up_level1", "up_coarse", "top", "down_coarse",
-                          "down_level1", "p_update")
+    PROFILE_CATEGORIES = ("spmv", "tile_up", "mid_up", "coarse", "mid_down", "tile_down",
+                          "unused6", "unused7")
 
     def set_profiling(self, on: bool = True):
         _check(_lib.msp_set_profiling(self._h, 1 if on else 0))

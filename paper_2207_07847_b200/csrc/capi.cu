@@ -125,6 +125,16 @@ int msp_info(const msp_handle* H, msp_info_t* out) {
     out->mwm_rounds = h.mwm_rounds;
     out->mu = h.mu;
     out->setup_ms = h.setup_ms;
+    int32_t tl = 1;
+    int64_t nt = 0;
+    for (const auto& T : h.tiers) {
+      if (!T.generic && T.k0 == 1) { tl = T.k1; nt = T.ntiles; }
+    }
+    out->tile_level = tl;
+    out->coarse_level = h.Kc;
+    out->ntiles = nt;
+    out->ntiers = (int32_t)h.tiers.size();
+    out->spmv_grid = (int32_t)h.spmv_grid;
   });
 }
 

@@ -9,10 +9,11 @@
 #include <vector>
 
 #include "../../include/msp_b200.h"
+#include "sched.cuh"
 
 namespace msp {
 
-enum { PC_SPMV = 0, PC_UPDATE, PC_UP1, PC_UPC, PC_TOP, PC_DOWNC, PC_DOWN1, PC_PUPD };
+enum { PC_SPMV = 0, PC_TILE_UP, PC_MID_UP, PC_COARSE, PC_MID_DOWN, PC_TILE_DOWN, PC_UNUSED6, PC_UNUSED7 };
 
 // ---------------------------------------------------------------- errors
 struct Error {
@@ -96,18 +97,56 @@ struct Handle {
   DBuf<double> w1;
   DBuf<int32_t> cptr;         // concatenated child pointers: level k block at cptr_off[k-1]
   std::vector<int64_t> cptr_off;
-  DBuf<double> c0, c1, c2;    // per expanded node (nested): block-tree factor data
+  // MSP block-tree factors, packed:
+  //   kinv[3 (off_{k+1} - n + B) + {0,1,2}] = K'^{-1} (uu, uv, vv) of aggregate B at level k+1
+  //   lof[3 (lo_off[k-1] + p - 2B - 2) + {0,1,2}] = (s w_xu / d, s w_xv / d, 1 / d) of leftover p
+  DBuf<double> kinv, lof;
+  std::vector<int64_t> lo_off;  // [l]: first leftover slot of the level-k children
   DBuf<double> Nsub;          // subtree sizes N_i (double)
   DBuf<double> gvec;          // g = K_S^{-1} N_S per node
+  DBuf<double> Hvec;          // [n]: gdot weights, gdot = (r, H)
   DBuf<double> top_pinv;      // dense (sigma_l L_l)^+ of the top level, nested order
   double c_sum = 0.0;         // sum_{k=1}^{l} (-mu)^{k-1}
   double GN = 0.0;            // sum over non-top nodes g_i N_i
   std::vector<double> neg_mu_pow;  // (-mu)^j, j = 0..l
 
+  // ---- level-1 Laplacian in SELL-32 (slices of 32 rows, column-major,
+  // padded with (self, 0)); rows of degree > LCAP are "long": empty in SELL,
+  // flagged in sell_mask and handled warp-per-row from the nested CSR
+  int64_t nslices = 0, nlong = 0;
+  DBuf<int64_t> sell_ptr;
+  DBuf<int32_t> sell_col;
+  DBuf<double> sell_w;
+  DBuf<uint32_t> sell_mask;
+  DBuf<int32_t> long_rows;
+
+  // ---- solve schedule: tiers of tile
+  // kernels over levels 1..Kc, then one single-CTA kernel for Kc..L
+  struct Tier {
+    int32_t k0 = 1, k1 = 1;
+    int64_t ntiles = 0;
+    DBuf<int32_t> tstart;     // [k1-k0+1][ntiles+1]: first level-(k0+t) node of tile j
+    size_t smem_up = 0, smem_down = 0;
+    bool generic = false;     // one level by per-node kernels (an aggregate too large to tile)
+  };
+  std::vector<Tier> tiers;
+  int32_t Kc = 1;
+  size_t coarse_smem = 0;
+  bool coarse_stage_pinv = false;
+  std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
+  unsigned spmv_grid = 1;
+
   // ---- solve workspaces
-  DBuf<double> Y, S, Z, W;    // n~-layout sweep vectors
+  DBuf<double> Y, Z, W;       // n~-layout sweep vectors (y = P^T sums, z, w)
   DBuf<double> red;           // reduction partials
   DBuf<double> vx, vr, vp, vq, vz, vb;  // PCG vectors (nested numbering)
+  DBuf<double> vp2;           // ping-pong partner of vp (p = z + beta p fused into L p)
+  int pparity = 0;            // which of vp / vp2 holds the current p
+  cudaGraphExec_t graph = nullptr;  // captured batch of PCG iterations
+  int graph_batch = 0;
+  int64_t graph_launches = 0;
+  cudaStream_t own_stream = nullptr;  // capture / replay stream of the graph
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf<unsigned int> counters;
   DBuf<double> scal;          // device scalars of PCG
   DBuf<double> stage_in, stage_out;   // host-mode staging
@@ -116,6 +155,14 @@ struct Handle {
   int profile = 0;            // bracket solve launches with events (msp_set_profiling)
   double prof_ms[MSP_PROF_NCAT] = {0};
   int64_t prof_cnt[MSP_PROF_NCAT] = {0};
+  Handle() = default;
+  Handle(const Handle&) = delete;
+  ~Handle() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
 };
 
 // setup.cu
@@ -131,5 +178,8 @@ void scatter_from_nested(Handle& h, const double* src_nested, double* dst_orig, 
 void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol, int maxit,
                 cudaStream_t st, msp_report* rep);
 void alloc_solve_workspace(Handle& h);
+void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
+Lv make_level_table(const Handle& h);              // setup.cu
+void release_graph(Handle& h);
 
 }  // namespace msp

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -275,15 +276,16 @@ __global__ void k_core_ids(int64_t n, const int32_t* __restrict__ mate, const in
 // leftovers into the pair gives  K' = [[q+e_u, -q], [-q, q+e_v]]  with
 //   d_x = a_x + sigma (w_xu + w_xv),  q = sigma w_uv + sum sigma^2 w_xu w_xv / d_x,
 //   e_u = a_u + sum sigma w_xu a_x / d_x,  e_v likewise
-// (all terms positive: no cancellation).  Stored per node (nested index):
-//   S[0]: (Kinv_uu, Kinv_uv, Kinv_vv);  leftover x: (sigma w_xu/d_x, sigma w_xv/d_x, 1/d_x).
+// (all terms positive: no cancellation).  Stored packed:
+//   kinv[3 (off_{k+1} - n + B) + (0,1,2)] = K'^{-1} (uu, uv, vv)
+//   lof[3 (lo_k + x - 2B - 2) + (0,1,2)]  = (sigma w_xu / d_x, sigma w_xv / d_x, 1 / d_x)
 // Also N_B = 1 + sum N_c (subtree sizes in T~) and g_S = K_S^{-1} N_S.
 __global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
                              const int32_t* __restrict__ order_k,   // nested pos -> canonical (level k)
                              const double* __restrict__ apar, const double* __restrict__ wa,
                              const double* __restrict__ wb, double sigma, int64_t off_k,
-                             int64_t off_k1, double* __restrict__ c0, double* __restrict__ c1,
-                             double* __restrict__ c2, double* __restrict__ Nsub,
+                             int64_t off_k1, int64_t n1, int64_t lo_k, double* __restrict__ kinv,
+                             double* __restrict__ lof, double* __restrict__ Nsub,
                              double* __restrict__ gvec, double* __restrict__ gN_part, int first_level) {
   int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (B >= nparent) return;
@@ -292,6 +294,7 @@ __global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
   const double au = apar[cu], av = apar[cv];
   const double wuv = wa[cu];
   double q = sigma * wuv, eu = au, ev = av;
+  const int64_t lb = 3 * (lo_k - 2 * B - 2);  // lof[lb + 3 x + j] for leftover child x
   for (int32_t p = s0 + 2; p < s1; ++p) {
     const int32_t x = order_k[p];
     const double ax = apar[x], wxu = sigma * wa[x], wxv = sigma * wb[x];
@@ -299,14 +302,14 @@ __global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
     q += wxu * wxv / d;
     eu += wxu * ax / d;
     ev += wxv * ax / d;
-    c0[off_k + p] = wxu / d;
-    c1[off_k + p] = wxv / d;
-    c2[off_k + p] = 1.0 / d;
+    lof[lb + 3 * (int64_t)p + 0] = wxu / d;
+    lof[lb + 3 * (int64_t)p + 1] = wxv / d;
+    lof[lb + 3 * (int64_t)p + 2] = 1.0 / d;
   }
   const double det = q * (eu + ev) + eu * ev;
   const double kuu = (q + ev) / det, kuv = q / det, kvv = (q + eu) / det;
-  c0[off_k + s0] = kuu; c1[off_k + s0] = kuv; c2[off_k + s0] = kvv;
-  c0[off_k + s0 + 1] = 0.0; c1[off_k + s0 + 1] = 0.0; c2[off_k + s0 + 1] = 0.0;
+  double* ki = kinv + 3 * (off_k1 - n1 + B);
+  ki[0] = kuu; ki[1] = kuv; ki[2] = kvv;
   // subtree sizes
   double NB = 1.0;
   for (int32_t p = s0; p < s1; ++p) {
@@ -320,8 +323,8 @@ __global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
   double tu = Nu, tv = Nv;
   for (int32_t p = s0 + 2; p < s1; ++p) {
     const double t = Nsub[off_k + p];
-    tu += c0[off_k + p] * t;
-    tv += c1[off_k + p] * t;
+    tu += lof[lb + 3 * (int64_t)p + 0] * t;
+    tv += lof[lb + 3 * (int64_t)p + 1] * t;
   }
   const double zu = kuu * tu + kuv * tv, zv = kuv * tu + kvv * tv;
   gvec[off_k + s0] = zu;
@@ -329,11 +332,59 @@ __global__ void k_msp_factor(int64_t nparent, const int32_t* __restrict__ cptr,
   double gN = zu * Nu + zv * Nv;
   for (int32_t p = s0 + 2; p < s1; ++p) {
     const double t = Nsub[off_k + p];
-    const double zx = c2[off_k + p] * t + c0[off_k + p] * zu + c1[off_k + p] * zv;
+    const double zx = lof[lb + 3 * (int64_t)p + 2] * t + lof[lb + 3 * (int64_t)p + 0] * zu + lof[lb + 3 * (int64_t)p + 1] * zv;
     gvec[off_k + p] = zx;
     gN += zx * t;
   }
   gN_part[B] = gN;
+}
+
+// gdot weights, top-down: G_k[c] = c(k) g_k[c] + G_{k+1}[parent(c)] (G_L = 0);
+// then sum_{non-top i} g_i s_i = sum_i g_i c(lev i) y_i = (r, G_1)
+__global__ void k_hvec(int64_t nB, const int32_t* __restrict__ cptr, const double* __restrict__ gk, double ckk,
+                       const double* __restrict__ Gpar, double* __restrict__ Gk) {
+  int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (B >= nB) return;
+  const double gp = Gpar ? Gpar[B] : 0.0;
+  for (int32_t c = cptr[B]; c < cptr[B + 1]; ++c) Gk[c] = ckk * gk[c] + gp;
+}
+
+// ------------------------------------------------------------ SELL-32
+__global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restrict__ rowptr, int lcap,
+                             int64_t* __restrict__ width, uint32_t* __restrict__ mask, int32_t* __restrict__ islong) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;  // warp-uniform
+  const int64_t r = s * 32 + lane;
+  int deg = 0;
+  if (r < n) deg = rowptr[r + 1] - rowptr[r];
+  const bool lng = deg > lcap;
+  if (r < n) islong[r] = lng ? 1 : 0;
+  int w = lng ? 0 : deg;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  const uint32_t m = __ballot_sync(0xffffffffu, lng);
+  if (lane == 0) { width[s] = 32 * (int64_t)w; mask[s] = m; }
+}
+
+__global__ void k_sell_fill(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
+                            const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            const double* __restrict__ w, const uint32_t* __restrict__ mask,
+                            int32_t* __restrict__ scol, double* __restrict__ sw) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int64_t r = s * 32 + lane;
+  const int64_t base = sptr[s];
+  const int64_t width = (sptr[s + 1] - base) / 32;
+  const bool lng = (mask[s] >> lane) & 1u;
+  int32_t e0 = 0, deg = 0;
+  if (r < n && !lng) { e0 = rowptr[r]; deg = rowptr[r + 1] - e0; }
+  for (int64_t k = 0; k < width; ++k) {
+    const int64_t idx = base + k * 32 + lane;
+    if (k < deg) { scol[idx] = col[e0 + k]; sw[idx] = w[e0 + k]; }
+    else { scol[idx] = (r < n) ? (int32_t)r : 0; sw[idx] = 0.0; }
+  }
 }
 
 // dense top-level Laplacian sigma_l L_l (top nested order == canonical order)
@@ -400,6 +451,38 @@ __global__ void k_top_pinv(int nt, const double* __restrict__ M, double* __restr
     const double g = (i < m && j < m) ? A[i * W + m + j] : 0.0;
     out[idx] = g - rmean[i] - cmean[j] + gmean;
   }
+}
+
+
+// ------------------------------------------------------------ solve schedule
+// first1_{k+1}[B] = first level-1 descendant of level-(k+1) node B (B <= n_{k+1})
+__global__ void k_first1(int64_t nB, const int32_t* __restrict__ cptr, const int32_t* __restrict__ f_in,
+                         int32_t* __restrict__ f_out, int* __restrict__ maxsz) {
+  int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (B > nB) return;
+  f_out[B] = f_in[cptr[B]];
+  if (B < nB) atomicMax(maxsz, f_in[cptr[B + 1]] - f_in[cptr[B]]);
+}
+
+// tile j starts at the first level-Kt node whose subtree starts at or after j*T
+__global__ void k_tile_bounds(int64_t ntiles, int64_t nK, int64_t T, const int32_t* __restrict__ first1,
+                              int32_t* __restrict__ bnd) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j > ntiles) return;
+  if (j == ntiles) { bnd[j] = (int32_t)nK; return; }
+  const int64_t target = j * T;
+  int64_t lo = 0, hi = nK;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (first1[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bnd[j] = (int32_t)lo;
+}
+
+__global__ void k_tile_descend(int64_t cnt, const int32_t* __restrict__ cptr, const int32_t* __restrict__ above,
+                               int32_t* __restrict__ below) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < cnt) below[j] = cptr[above[j]];
 }
 
 // ------------------------------------------------------------ validation
@@ -618,7 +701,8 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
   h.cptr_off.assign(L, 0);
   int64_t cptr_total = 0;
   for (int k = 1; k < L; ++k) { h.cptr_off[k - 1] = cptr_total; cptr_total += h.lv[k].n + 1; }
-  h.cptr.alloc(std::max<int64_t>(cptr_total, 1));
+  h.cptr.alloc(cptr_total + 8);  // + padding: TMA windows are rounded to 16 B
+  MSP_CUDA(cudaMemsetAsync(h.cptr.p, 0, (cptr_total + 8) * sizeof(int32_t), st));
   for (int k = L - 1; k >= 1; --k) {
     const int64_t nk = h.lv[k - 1].n;
     DBuf<uint64_t> keys, skeys;
@@ -655,12 +739,19 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
 
   // ---- MSP block-tree factors, bottom-up
   const int64_t nt = h.n_tilde;
-  h.c0.alloc(nt); h.c1.alloc(nt); h.c2.alloc(nt);
-  h.Nsub.alloc(nt); h.gvec.alloc(nt);
-  MSP_CUDA(cudaMemsetAsync(h.c0.p, 0, nt * sizeof(double), st));
-  MSP_CUDA(cudaMemsetAsync(h.c1.p, 0, nt * sizeof(double), st));
-  MSP_CUDA(cudaMemsetAsync(h.c2.p, 0, nt * sizeof(double), st));
-  MSP_CUDA(cudaMemsetAsync(h.gvec.p, 0, nt * sizeof(double), st));
+  h.lo_off.assign(L, 0);
+  {
+    int64_t lo = 0;
+    for (int k = 1; k < L; ++k) { h.lo_off[k - 1] = lo; lo += h.lv[k - 1].n - 2 * h.lv[k].n; }
+    h.lo_off[L - 1] = lo;
+    h.lof.alloc(3 * lo + 8);
+    MSP_CUDA(cudaMemsetAsync(h.lof.p, 0, (3 * lo + 8) * sizeof(double), st));
+  }
+  h.kinv.alloc(3 * (nt - n) + 8);
+  MSP_CUDA(cudaMemsetAsync(h.kinv.p, 0, (3 * (nt - n) + 8) * sizeof(double), st));
+  h.Nsub.alloc(nt + 8); h.gvec.alloc(nt + 8);
+  MSP_CUDA(cudaMemsetAsync(h.Nsub.p, 0, (nt + 8) * sizeof(double), st));
+  MSP_CUDA(cudaMemsetAsync(h.gvec.p, 0, (nt + 8) * sizeof(double), st));
   h.apar_canon.clear();
   h.apar_canon.resize(L > 1 ? L - 1 : 0);
   double GN = 0.0;
@@ -678,12 +769,65 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
                                                  wa.p, wb.p);
     k_msp_factor<<<grid_for(nk1), TPB, 0, st>>>(nk1, h.cptr.p + h.cptr_off[k - 1], order[k - 1].p,
                                                 h.apar_canon[k - 1].p, wa.p, wb.p, mu_pow[2 * (k - 1)],
-                                                h.lv[k - 1].off, h.lv[k].off, h.c0.p, h.c1.p, h.c2.p,
-                                                h.Nsub.p, h.gvec.p, gpart.p, k == 1 ? 1 : 0);
+                                                h.lv[k - 1].off, h.lv[k].off, n, h.lo_off[k - 1], h.kinv.p,
+                                                h.lof.p, h.Nsub.p, h.gvec.p, gpart.p, k == 1 ? 1 : 0);
     MSP_LAUNCH_CHECK();
     GN += reduce_sum(tmp, gpart.p, nk1, st);
   }
   h.GN = GN;
+
+  // ---- gdot weights H = G_1 (top-down over the hierarchy)
+  {
+    std::vector<double> ckv(L + 1, 0.0);
+    double c = 0.0, pw = 1.0;
+    for (int k = 1; k <= L; ++k) { c += pw; pw *= -h.mu; ckv[k] = c; }
+    DBuf<double> G;
+    G.alloc(nt);
+    MSP_CUDA(cudaMemsetAsync(G.p, 0, nt * sizeof(double), st));
+    for (int k = L - 1; k >= 1; --k)
+      k_hvec<<<grid_for(h.lv[k].n), TPB, 0, st>>>(h.lv[k].n, h.cptr.p + h.cptr_off[k - 1], h.gvec.p + h.lv[k - 1].off,
+                                                   ckv[k], (k + 1 < L) ? G.p + h.lv[k].off : nullptr,
+                                                   G.p + h.lv[k - 1].off);
+    MSP_LAUNCH_CHECK();
+    h.Hvec.alloc(n + 8);
+    MSP_CUDA(cudaMemsetAsync(h.Hvec.p, 0, (n + 8) * sizeof(double), st));
+    MSP_CUDA(cudaMemcpyAsync(h.Hvec.p, G.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    MSP_CUDA(cudaStreamSynchronize(st));
+  }
+
+  // ---- level-1 Laplacian in SELL-32 for the solve
+  {
+    int lcap = 64;
+    if (const char* e = std::getenv("MSP_SELL_LCAP")) lcap = std::max(1, std::atoi(e));
+    const int64_t ns = (n + 31) / 32;
+    h.nslices = ns;
+    DBuf<int64_t> width;
+    DBuf<int32_t> islong;
+    width.alloc(ns + 1);
+    islong.alloc(n);
+    h.sell_mask.alloc(ns);
+    h.sell_ptr.alloc(ns + 1);
+    MSP_CUDA(cudaMemsetAsync(width.p + ns, 0, sizeof(int64_t), st));
+    k_sell_width<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.rowptr1.p, lcap, width.p, h.sell_mask.p, islong.p);
+    MSP_LAUNCH_CHECK();
+    exclusive_scan(tmp, width.p, h.sell_ptr.p, ns + 1, st);
+    const int64_t tot = d2h_scalar(h.sell_ptr.p + ns, st);
+    h.sell_col.alloc(std::max<int64_t>(tot, 1));
+    h.sell_w.alloc(std::max<int64_t>(tot, 1));
+    k_sell_fill<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.sell_ptr.p, h.rowptr1.p, h.col1.p, h.w1.p,
+                                                   h.sell_mask.p, h.sell_col.p, h.sell_w.p);
+    MSP_LAUNCH_CHECK();
+    // long rows, in increasing order (deterministic)
+    DBuf<int32_t> ids, nsel;
+    ids.alloc(n);
+    nsel.alloc(1);
+    k_iota32<<<grid_for(n), TPB, 0, st>>>(n, ids.p);
+    h.long_rows.alloc(n);
+    size_t bytes = 0;
+    MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, islong.p, h.long_rows.p, nsel.p, n, st));
+    MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, islong.p, h.long_rows.p, nsel.p, n, st));
+    h.nlong = d2h_scalar(nsel.p, st);
+  }
 
   // ---- top level: dense pseudo-inverse of sigma_l L_l
   {
@@ -702,6 +846,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     MSP_CUDA(cudaStreamSynchronize(st));
   }
 
+  build_schedule(h, st);
   MSP_CUDA(cudaEventRecord(e1, st));
   MSP_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -711,6 +856,161 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
   cudaEventDestroy(e1);
   h.mates_canon = std::move(mates);
   h.order_nested = std::move(order);
+}
+
+
+Lv make_level_table(const Handle& h) {
+  Lv lv{};
+  lv.L = h.levels;
+  lv.Kc = h.Kc;
+  for (int k = 1; k <= h.levels; ++k) {
+    lv.n[k - 1] = h.lv[k - 1].n;
+    lv.off[k - 1] = h.lv[k - 1].off;
+    lv.cpo[k - 1] = (k < h.levels) ? h.cptr_off[k - 1] : 0;
+    lv.lo[k - 1] = h.lo_off.empty() ? 0 : h.lo_off[k - 1];
+    lv.ck[k] = h.ck.empty() ? 0.0 : h.ck[k];
+  }
+  lv.negmu = -h.mu;
+  lv.c_sum = h.c_sum;
+  lv.n_tilde = (double)h.n_tilde;
+  lv.GN = h.GN;
+  return lv;
+}
+
+// Tiers and tiles of the solve schedule.
+void build_schedule(Handle& h, cudaStream_t st) {
+  const int L = h.levels;
+  if (L >= MAXL) throw Error{MSP_ERR_UNSUPPORTED, "more than 39 levels"};
+  h.ck.assign(L + 1, 0.0);
+  {
+    double c = 0.0, pw = 1.0;
+    for (int k = 1; k <= L; ++k) { c += pw; pw *= -h.mu; h.ck[k] = c; }
+  }
+  int64_t T = 512, SUB = 256, CMAX = 2048;
+  if (const char* e = std::getenv("MSP_TILE_T")) T = std::max<int64_t>(16, std::atoll(e));
+  SUB = T / 2;
+  if (const char* e = std::getenv("MSP_TILE_SUB")) SUB = std::max<int64_t>(2, std::atoll(e));
+  if (const char* e = std::getenv("MSP_COARSE_MAX")) CMAX = std::max<int64_t>(2, std::atoll(e));
+  const size_t SMEM_CAP = 200 * 1024;
+  const Lv lv = make_level_table(h);
+
+  // coarse level: smallest Kc whose levels Kc..L fit the single-CTA kernel
+  h.coarse_stage_pinv = h.lv[L - 1].n <= 32;
+  {
+    int Kc = L;
+    int64_t tail = 0;
+    for (int k = L; k >= 1; --k) {
+      tail += h.lv[k - 1].n;
+      if (tail > CMAX) break;
+      Lv t = lv;
+      t.Kc = k;
+      CoarseLayout C;
+      if ((size_t)coarse_layout(t, h.coarse_stage_pinv, C) > SMEM_CAP) break;
+      Kc = k;
+    }
+    h.Kc = Kc;
+  }
+  Lv lvc = lv;
+  lvc.Kc = h.Kc;
+  {
+    CoarseLayout C;
+    h.coarse_smem = (size_t)coarse_layout(lvc, h.coarse_stage_pinv, C);
+  }
+
+  // tiers over levels 1..Kc
+  h.tiers.clear();
+  int k0 = 1;
+  auto add_tiles = [&](int k0_, int k1_, DBuf<int32_t>* first_k1) {
+    Handle::Tier t;
+    t.k0 = k0_;
+    t.k1 = k1_;
+    const int nl = k1_ - k0_ + 1;
+    const int64_t n0 = h.lv[k0_ - 1].n;
+    t.ntiles = std::max<int64_t>(1, (n0 + T - 1) / T);
+    const int64_t nt1 = t.ntiles + 1;
+    t.tstart.alloc((size_t)nl * nt1);
+    if (nl == 1) {
+      DBuf<int32_t> id;
+      id.alloc(n0 + 1);
+      k_iota32<<<grid_for(n0 + 1), TPB, 0, st>>>(n0 + 1, id.p);
+      k_tile_bounds<<<grid_for(nt1), TPB, 0, st>>>(t.ntiles, n0, T, id.p, t.tstart.p);
+      MSP_LAUNCH_CHECK();
+      MSP_CUDA(cudaStreamSynchronize(st));
+      t.smem_up = 0;  // level 1 only: nothing staged
+    } else {
+      k_tile_bounds<<<grid_for(nt1), TPB, 0, st>>>(t.ntiles, h.lv[k1_ - 1].n, T, first_k1->p,
+                                                    t.tstart.p + (int64_t)(nl - 1) * nt1);
+      for (int u = nl - 2; u >= 0; --u) {
+        const int kc = k0_ + u;  // child level
+        k_tile_descend<<<grid_for(nt1), TPB, 0, st>>>(nt1, h.cptr.p + h.cptr_off[kc - 1],
+                                                       t.tstart.p + (int64_t)(u + 1) * nt1,
+                                                       t.tstart.p + (int64_t)u * nt1);
+      }
+      MSP_LAUNCH_CHECK();
+      std::vector<int32_t> ts((size_t)nl * nt1);
+      MSP_CUDA(cudaMemcpyAsync(ts.data(), t.tstart.p, ts.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+      int64_t a[MAXT], b[MAXT];
+      for (int64_t j = 0; j < t.ntiles; ++j) {
+        for (int u = 0; u < nl; ++u) { a[u] = ts[(size_t)u * nt1 + j]; b[u] = ts[(size_t)u * nt1 + j + 1]; }
+        TileLayout D;
+        TileLayoutUp U;
+        t.smem_down = std::max(t.smem_down, (size_t)tile_layout_down(lvc, k0_, nl, a, b, D));
+        t.smem_up = std::max(t.smem_up, (size_t)tile_layout_up(lvc, k0_, nl, a, b, U));
+      }
+    }
+    h.tiers.push_back(std::move(t));
+  };
+  if (h.Kc == 1) {
+    add_tiles(1, 1, nullptr);  // the PCG update only; everything else in the coarse kernel
+  }
+  while (k0 < h.Kc) {
+    // first level-k0 descendants of the levels above, and the largest subtree
+    const int kmax = std::min(h.Kc, k0 + MAXT - 1);
+    std::vector<DBuf<int32_t>> first(kmax - k0 + 1);
+    first[0].alloc(h.lv[k0 - 1].n + 1);
+    k_iota32<<<grid_for(h.lv[k0 - 1].n + 1), TPB, 0, st>>>(h.lv[k0 - 1].n + 1, first[0].p);
+    DBuf<int> mx;
+    mx.alloc(kmax - k0 + 1);
+    MSP_CUDA(cudaMemsetAsync(mx.p, 0, (kmax - k0 + 1) * sizeof(int), st));
+    for (int k = k0 + 1; k <= kmax; ++k) {
+      const int u = k - k0;
+      first[u].alloc(h.lv[k - 1].n + 1);
+      k_first1<<<grid_for(h.lv[k - 1].n + 1), TPB, 0, st>>>(h.lv[k - 1].n, h.cptr.p + h.cptr_off[k - 2],
+                                                           first[u - 1].p, first[u].p, mx.p + u);
+    }
+    MSP_LAUNCH_CHECK();
+    std::vector<int> maxsz(kmax - k0 + 1);
+    MSP_CUDA(cudaMemcpyAsync(maxsz.data(), mx.p, maxsz.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    MSP_CUDA(cudaStreamSynchronize(st));
+    int k1 = k0;
+    for (int k = k0 + 1; k <= kmax; ++k) {
+      if (maxsz[k - k0] <= SUB) k1 = k;
+      else break;
+    }
+    if (k1 == k0) {  // an aggregate with more than SUB children: one generic level
+      Handle::Tier t;
+      t.k0 = k0;
+      t.k1 = k0 + 1;
+      t.generic = true;
+      h.tiers.push_back(std::move(t));
+      if (k0 == 1) {  // the PCG update still needs a tile pass over level 1
+        add_tiles(1, 1, nullptr);
+        std::swap(h.tiers[h.tiers.size() - 1], h.tiers[h.tiers.size() - 2]);
+      }
+      k0 += 1;
+      continue;
+    }
+    for (;;) {  // shrink the tier until its tiles fit in shared memory
+      add_tiles(k0, k1, &first[k1 - k0]);
+      if (h.tiers.back().smem_down <= SMEM_CAP || k1 == k0 + 1) break;
+      h.tiers.pop_back();
+      --k1;
+    }
+    if (h.tiers.back().smem_down > SMEM_CAP)
+      throw Error{MSP_ERR_UNSUPPORTED, "a tile does not fit in shared memory"};
+    k0 = k1;
+  }
 }
 
 }  // namespace msp

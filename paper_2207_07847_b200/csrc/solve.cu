@@ -1,13 +1,34 @@
 // solve.cu -- solve phase of the PEGP/MSP solver (sm_100a): apply_L, the
-// exact MSP apply R = P(mu) L_T~^+ P(mu)^T as level-ordered restrict /
-// prolong sweeps over the nested aggregate hierarchy, and fused PCG.
+// exact MSP apply R = P(mu) L_T~^+ P(mu)^T, and fused PCG.
 //
 // Layout (nested numbering): level-k node i of the
 // expanded graph lives at index off_k + i of every n~-vector; the children of
 // level-(k+1) node B are level-k nodes cptr_k[B] .. cptr_k[B+1]-1, the first
-// two being the matched pair, the rest leftovers.
+// two being the matched pair, the rest leftovers.  Every aggregate of every
+// level is a contiguous range of the level below, and so is every subtree:
+// the MSP sweeps run as tiers of tile kernels (one CTA per tile of whole
+// subtrees; all intermediate levels in shared memory, staged with TMA bulk
+// copies), then one single-CTA kernel for the coarse levels Kc..L.
+//
+// Arithmetic of R r, with y_1 = r, y_{k+1} = P^T y_k
+// (sums over children) and c(k) = sum_{j<k} (-mu)^j:
+//   r~ = P(mu)^T r has level-k block (-mu)^{k-1} y_k, and its subtree sums in
+//   T~ are s_k = c(k) y_k;
+//   rho = c(L) sum(r) / n~ projects r~ off the ones vector;
+//   top:   z_L = (sigma_L L_L)^+ (s_L - rho N_L), then shifted so that z~ has
+//          zero mean: m = (N_L . z_L + gdot - rho GN) / n~ with
+//          gdot = sum_{non-top} g_i s_i = (r, H);
+//   down:  per aggregate, zeta = K_S^{-1} (s_S - rho N_S) (pair + leftover
+//          elimination), z_c = z_B + zeta_c;
+//   out:   w_L = z_L, w_k = z_k + (-mu) P w_{k+1}; R r = w_1.
+//
+// Every kernel of an iteration is launched with programmatic dependent launch
+// (PDL): its prologue (tile ranges, shared-memory layout, TMA of constant
+// data) overlaps the tail of the previous kernel; griddepcontrol.wait guards
+// the first read of anything the previous kernel wrote.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -15,61 +36,163 @@ namespace msp {
 
 namespace {
 
-constexpr int TPB = 256;
+constexpr int TPB = 256;      // SpMV and per-node kernels
+constexpr int TT = 256;       // tile kernels
+constexpr int CT = 1024;      // coarse kernel (single CTA)
 
 // device scalar slots
-enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_NSCAL };
+enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S_NSCAL };
 // counter slots
 enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
+// sweep modes
+enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2 };
 
 inline unsigned grid_for(int64_t n, int tpb = TPB) {
   int64_t g = (n + tpb - 1) / tpb;
   return (unsigned)std::max<int64_t>(g, 1);
 }
 
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void stage_issue(const Seg& s, char* sm, const void* src, int es, uint64_t* bar) {
+  if (s.nbytes > 0) tma_1d(sm + s.soff, (const char*)src + s.gstart * es, (uint32_t)s.nbytes, bar);
+}
+
+template <typename T>
+__device__ __forceinline__ T* seg_ptr(char* sm, const Seg& s) {
+  return reinterpret_cast<T*>(sm + s.soff);
+}
+
+// ------------------------------------------------------------ reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// block-wide sum; result valid in thread 0
+// block-wide sum, result valid in every thread
 template <int NT>
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double ws[NT / 32];
+  __shared__ double tot;
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
   if (lane == 0) ws[wid] = v;
   __syncthreads();
-  double t = 0.0;
   if (wid == 0) {
-    t = (lane < NT / 32) ? ws[lane] : 0.0;
+    double t = (lane < NT / 32) ? ws[lane] : 0.0;
     t = warp_sum(t);
+    if (lane == 0) tot = t;
   }
   __syncthreads();
-  return t;
+  return tot;
 }
 
-// deterministic sum of partials[0..n) by one block; result in thread 0
+// deterministic sum of partials[0..n) written by other blocks (L2 reads)
 template <int NT>
-__device__ __forceinline__ double block_sum_array(const double* part, int64_t n) {
+__device__ __forceinline__ double block_sum_partials(const double* part, int64_t n) {
   double v = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += NT) v += part[i];
+  for (int64_t i = threadIdx.x; i < n; i += NT) v += __ldcg(part + i);
   return block_sum<NT>(v);
 }
 
-// "last block done" ticket: returns true in every thread of the last block
+// "last block done" ticket after thread 0 wrote this block's partial(s)
 __device__ __forceinline__ bool last_block(unsigned int* counter) {
   __shared__ bool is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned t = atomicAdd(counter, 1u);
     is_last = (t == gridDim.x - 1);
+    if (is_last) __threadfence();
   }
   __syncthreads();
-  if (is_last) __threadfence();
   return is_last;
+}
+
+// Exact solve of one aggregate of T~: children [s0, s1) (matched pair s0,
+// s0+1, leftovers s0+2..), K(j) the packed K'^{-1} (uu, uv, vv), C(p, j) the
+// leftover coefficients (sigma w_xu / d, sigma w_xv / d, 1 / d):
+// zeta = K_S^{-1} t, emitted as ef(p, z_B + zeta_p, z_B + zeta_p + wbm).
+template <typename TF, typename KF, typename CF, typename EF>
+__device__ __forceinline__ void block_solve(int64_t s0, int64_t s1, KF K, CF C, double zb, double wbm, TF tf,
+                                            EF ef) {
+  const double tu = tf(s0), tv = tf(s0 + 1);
+  double au = tu, av = tv;
+  for (int64_t p = s0 + 2; p < s1; ++p) {
+    const double tx = tf(p);
+    au += C(p, 0) * tx;
+    av += C(p, 1) * tx;
+  }
+  const double kuu = K(0), kuv = K(1), kvv = K(2);
+  const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
+  { const double z = zb + zu; ef(s0, z, z + wbm); }
+  { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
+  for (int64_t p = s0 + 2; p < s1; ++p) {
+    const double tx = tf(p);
+    const double zx = C(p, 2) * tx + C(p, 0) * zu + C(p, 1) * zv;
+    const double z = zb + zx;
+    ef(p, z, z + wbm);
+  }
+}
+
+// PCG scalars after the level-1 output: rz = (r, R r)
+__device__ __forceinline__ void finish_rz(double rz, double* scal, int mode) {
+  if (mode == M_ITER) scal[S_BETA] = rz / scal[S_RHO];
+  else scal[S_BETA] = 0.0;
+  scal[S_RHO] = rz;
+}
+
+// (r, r) and the convergence test (reading R10)
+__device__ __forceinline__ void finish_rr(double rr, double* scal, unsigned* cnt, int mode) {
+  scal[S_RR] = rr;
+  if (mode == M_INIT) {
+    scal[S_BB] = rr;
+    scal[S_TOL2] = scal[S_RTOL2] * rr;
+  } else {
+    cnt[C_IT] += 1;
+  }
+  if (rr <= scal[S_TOL2]) cnt[C_DONE] = 1;
 }
 
 // ----------------------------------------------------------------- permute
@@ -86,329 +209,587 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ perm, const dou
 }
 
 // ------------------------------------------------------------------ L_G x
-// y_i = sum_j w_ij (x_i - x_j)   (L_G = B^T W B, §2.1)
-// LANES threads per row; optional fused dot (x, y) -> alpha = rho / (p, Lp).
-template <int LANES, bool DOT>
-__global__ void __launch_bounds__(TPB) k_spmv(int64_t n, const int32_t* __restrict__ rowptr,
-                                              const int32_t* __restrict__ col,
-                                              const double* __restrict__ w,
-                                              const double* __restrict__ x, double* __restrict__ y,
+// y_i = sum_j w_ij (x_i - x_j)   (L_G = B^T W B, §2.1), SELL-32.
+// PCG: p = z + beta p_old (rows and gathered neighbours alike), q = L_G p,
+// (p, q) -> alpha = rho / (p, q); and the deferred x += alpha_prev p_old.
+template <bool PCG>
+__global__ void __launch_bounds__(TPB) k_spmv(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
+                                              const int32_t* __restrict__ scol, const double* __restrict__ sw,
+                                              const uint32_t* __restrict__ smask, int64_t nlong,
+                                              const int32_t* __restrict__ long_rows,
+                                              const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                              const double* __restrict__ w, const double* __restrict__ z,
+                                              const double* __restrict__ pold, double* __restrict__ pnew,
+                                              double* __restrict__ q, double* __restrict__ x,
                                               double* __restrict__ part, double* __restrict__ scal,
                                               unsigned int* __restrict__ cnt) {
-  if (DOT && cnt[C_DONE]) return;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t row = gid / LANES;
-  const int lane = threadIdx.x % LANES;
-  double acc = 0.0, xi = 0.0;
-  if (row < n) {
-    xi = x[row];
-    const int32_t e0 = rowptr[row], e1 = rowptr[row + 1];
-    for (int32_t e = e0 + lane; e < e1; e += LANES) acc += w[e] * (xi - x[col[e]]);
-  }
-#pragma unroll
-  for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  pdl_wait();
+  if (PCG && cnt[C_DONE]) return;
+  const double beta = PCG ? scal[S_BETA] : 0.0;
+  const double alpha = PCG ? scal[S_ALPHA] : 0.0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)TPB + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * TPB) >> 5;
   double d = 0.0;
-  if (row < n && lane == 0) {
-    y[row] = acc;
-    d = xi * acc;
+  for (int64_t s = warp; s < nslices; s += nwarps) {
+    const int64_t r = s * 32 + lane;
+    const bool valid = r < n;
+    const bool lng = (smask[s] >> lane) & 1u;
+    const int64_t base = sptr[s];
+    const int64_t width = (sptr[s + 1] - base) >> 5;
+    double pi = 0.0, po = 0.0;
+    if (valid) {
+      if (PCG) { po = pold[r]; pi = z[r] + beta * po; }
+      else pi = z[r];
+    }
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t k = 0; k < width; ++k) {
+      const int64_t idx = base + k * 32 + lane;
+      const int32_t j = scol[idx];
+      const double pj = PCG ? z[j] + beta * pold[j] : z[j];
+      acc += sw[idx] * (pi - pj);
+    }
+    if (valid && !lng) {
+      q[r] = acc;
+      if (PCG) {
+        pnew[r] = pi;
+        x[r] += alpha * po;
+        d += pi * acc;
+      }
+    }
   }
-  if (DOT) {
-    const double bs = block_sum<TPB>(d);
-    if (threadIdx.x == 0) part[blockIdx.x] = bs;
-    if (last_block(&cnt[C_SPMV])) {
-      const double pq = block_sum_array<TPB>(part, gridDim.x);
+  for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
+    const int64_t r = long_rows[i];
+    const double po = PCG ? pold[r] : 0.0;
+    const double pi = PCG ? z[r] + beta * po : z[r];
+    double acc = 0.0;
+    for (int32_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+      const int32_t j = col[e];
+      const double pj = PCG ? z[j] + beta * pold[j] : z[j];
+      acc += w[e] * (pi - pj);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      q[r] = acc;
+      if (PCG) {
+        pnew[r] = pi;
+        x[r] += alpha * po;
+        d += pi * acc;
+      }
+    }
+  }
+  if (!PCG) return;
+  pdl_trigger();
+  const double bs = block_sum<TPB>(d);
+  if (threadIdx.x == 0) part[blockIdx.x] = bs;
+  if (last_block(&cnt[C_SPMV])) {
+    const double pq = block_sum_partials<TPB>(part, gridDim.x);
+    if (threadIdx.x == 0) {
+      scal[S_PQ] = pq;
+      scal[S_ALPHA] = scal[S_RHO] / pq;
+      cnt[C_SPMV] = 0;
+    }
+  }
+}
+
+// x += alpha p for the last direction (the in-loop updates are deferred into
+// the next L p); p is the buffer the C_IT-th product wrote
+__global__ void k_x_final(int64_t n, double* __restrict__ x, const double* __restrict__ vp,
+                          const double* __restrict__ vp2, const double* __restrict__ scal,
+                          const unsigned* __restrict__ cnt) {
+  pdl_wait();
+  const unsigned it = cnt[C_IT];
+  if (it == 0) return;
+  const double* p = (it & 1u) ? vp2 : vp;
+  const double alpha = scal[S_ALPHA];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += alpha * p[i];
+}
+
+// ------------------------------------------------------------ tile up-sweep
+// Tier k0..k1 (nl = k1-k0+1 levels), one CTA per tile.  FIRST (k0 == 1):
+// level 1 is the PCG update r -= alpha q (mode ITER) with (r, r) and
+// gdot = (r, H); otherwise y_k0 is staged from Y.  Levels k0+1..k1:
+// y = P^T y in shared memory; y_k1 to global Y.
+template <bool FIRST>
+__global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, int k0, int nl, int ntiles,
+                                                const int32_t* __restrict__ tstart, const int32_t* __restrict__ cptr,
+                                                const double* __restrict__ q, double* __restrict__ r,
+                                                const double* __restrict__ H, double* __restrict__ Yg,
+                                                double* __restrict__ part_rr, double* __restrict__ part_gd,
+                                                double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ TileLayoutUp Ls;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t sa[MAXT], sb[MAXT];
+  __shared__ int sdone;
+  const int tile = blockIdx.x, nt1 = ntiles + 1;
+  if (threadIdx.x < nl) {
+    sa[threadIdx.x] = tstart[threadIdx.x * nt1 + tile];
+    sb[threadIdx.x] = tstart[threadIdx.x * nt1 + tile + 1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tile_layout_up(lv, k0, nl, sa, sb, Ls);
+    mbar_init(&bar, 1);
+    uint32_t cb = 0;
+    for (int t = 1; t < nl; ++t) cb += Ls.cp[t].nbytes;
+    if (cb) mbar_expect_tx(&bar, cb);
+    for (int t = 1; t < nl; ++t) stage_issue(Ls.cp[t], sm, cptr, 4, &bar);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    sdone = (mode == M_ITER) ? (int)cnt[C_DONE] : 0;
+    if (!FIRST && !sdone && Ls.y0.nbytes) {
+      mbar_expect_tx(&bar, Ls.y0.nbytes);
+      stage_issue(Ls.y0, sm, Yg, 8, &bar);
+    }
+    mbar_arrive(&bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (sdone) return;
+
+  double rr = 0.0, gd = 0.0;
+  if (FIRST) {
+    const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
+    const int64_t a1 = sa[0], n1 = sb[0] - sa[0];
+    double* y0 = seg_ptr<double>(sm, Ls.y0);
+    for (int64_t i = threadIdx.x; i < n1; i += TT) {
+      const int64_t gi = a1 + i;
+      double ri = r[gi];
+      if (mode == M_ITER) {
+        ri -= alpha * q[gi];
+        r[gi] = ri;
+      }
+      rr += ri * ri;
+      gd += H[gi] * ri;
+      if (nl > 1) y0[i] = ri;
+    }
+  }
+  for (int t = 1; t < nl; ++t) {  // child level k0+t-1, parent level k0+t
+    __syncthreads();
+    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t]);
+    const int64_t cpo = Ls.cp[t].org;
+    const double* yc = seg_ptr<double>(sm, t == 1 ? Ls.y0 : Ls.y[t - 1]);
+    const int64_t yco = (t == 1) ? Ls.y0.org : Ls.y[t - 1].org;
+    const bool last = (t == nl - 1);
+    double* yp = last ? Yg + lv.off[k0 + t - 1] : seg_ptr<double>(sm, Ls.y[t]);
+    const int64_t ypo = last ? 0 : Ls.y[t].org;
+    for (int64_t B = sa[t] + threadIdx.x; B < sb[t]; B += TT) {
+      const int32_t c0 = cp[B - cpo], c1 = cp[B + 1 - cpo];
+      double y = 0.0;
+      for (int32_t c = c0; c < c1; ++c) y += yc[c - yco];
+      yp[B - ypo] = y;
+    }
+  }
+  pdl_trigger();
+  if (FIRST) {
+    rr = block_sum<TT>(rr);
+    gd = block_sum<TT>(gd);
+    if (threadIdx.x == 0) { part_rr[tile] = rr; part_gd[tile] = gd; }
+    if (mode != M_APPLY && last_block(&cnt[C_UPD])) {
+      const double tot = block_sum_partials<TT>(part_rr, gridDim.x);
       if (threadIdx.x == 0) {
-        scal[S_PQ] = pq;
-        scal[S_ALPHA] = scal[S_RHO] / pq;
-        cnt[C_SPMV] = 0;
+        finish_rr(tot, scal, cnt, mode);
+        cnt[C_UPD] = 0;
       }
     }
   }
 }
 
-// x += alpha p ; r -= alpha q ; rr = (r, r) -> convergence flag
-__global__ void __launch_bounds__(TPB) k_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
-                                                const double* __restrict__ p, const double* __restrict__ q,
-                                                double* __restrict__ part, double* __restrict__ scal,
-                                                unsigned int* __restrict__ cnt) {
-  if (cnt[C_DONE]) return;
-  const double alpha = scal[S_ALPHA];
+// ---------------------------------------------------------- tile down-sweep
+// Tier k0..k1: recompute y (and subtree sizes N) of levels k0+1..k1-1 from
+// y_k0, read z, w at level k1, solve / prolong down to level k0.  FIRST: the
+// output R r and the partial (r, R r); otherwise z, w at level k0 to global.
+template <bool FIRST>
+__global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv, int k0, int nl, int ntiles,
+                                                  const int32_t* __restrict__ tstart, const int32_t* __restrict__ cptr,
+                                                  const double* __restrict__ kinv, const double* __restrict__ lof,
+                                                  const double* __restrict__ Nsub, const double* __restrict__ y0src,
+                                                  double* __restrict__ Zg, double* __restrict__ Wg,
+                                                  double* __restrict__ zout, double* __restrict__ part,
+                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ TileLayout Ls;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t sa[MAXT], sb[MAXT];
+  __shared__ int sdone;
+  const int tile = blockIdx.x, nt1 = ntiles + 1;
+  if (threadIdx.x < nl) {
+    sa[threadIdx.x] = tstart[threadIdx.x * nt1 + tile];
+    sb[threadIdx.x] = tstart[threadIdx.x * nt1 + tile + 1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tile_layout_down(lv, k0, nl, sa, sb, Ls);
+    mbar_init(&bar, 1);
+    uint32_t cb = Ls.n0.nbytes;
+    for (int t = 1; t < nl; ++t) cb += Ls.cp[t].nbytes + Ls.ki[t].nbytes;
+    for (int t = 0; t + 1 < nl; ++t) cb += Ls.lo[t].nbytes;
+    if (cb) mbar_expect_tx(&bar, cb);
+    for (int t = 1; t < nl; ++t) {
+      stage_issue(Ls.cp[t], sm, cptr, 4, &bar);
+      stage_issue(Ls.ki[t], sm, kinv, 8, &bar);
+    }
+    for (int t = 0; t + 1 < nl; ++t) stage_issue(Ls.lo[t], sm, lof, 8, &bar);
+    if (!FIRST) stage_issue(Ls.n0, sm, Nsub, 8, &bar);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+    if (!sdone) {
+      const uint32_t db = Ls.y0.nbytes + Ls.zt.nbytes + Ls.wt.nbytes;
+      if (db) mbar_expect_tx(&bar, db);
+      stage_issue(Ls.y0, sm, y0src, 8, &bar);
+      stage_issue(Ls.zt, sm, Zg, 8, &bar);
+      stage_issue(Ls.wt, sm, Wg, 8, &bar);
+    }
+    mbar_arrive(&bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (sdone) return;
+
+  // ---- recompute y and N of levels k0+1 .. k1-1
+  for (int t = 1; t + 1 < nl; ++t) {
+    __syncthreads();
+    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t]);
+    const int64_t cpo = Ls.cp[t].org;
+    const Seg& ycs = (t == 1) ? Ls.y0 : Ls.y[t - 1];
+    const double* yc = seg_ptr<double>(sm, ycs);
+    const double* nc = (t == 1) ? (FIRST ? nullptr : seg_ptr<double>(sm, Ls.n0)) : seg_ptr<double>(sm, Ls.nn[t - 1]);
+    const int64_t nco = (t == 1) ? Ls.n0.org : Ls.nn[t - 1].org;
+    double* yp = seg_ptr<double>(sm, Ls.y[t]);
+    double* np = seg_ptr<double>(sm, Ls.nn[t]);
+    const int64_t po = Ls.y[t].org;
+    for (int64_t B = sa[t] + threadIdx.x; B < sb[t]; B += TT) {
+      const int32_t c0 = cp[B - cpo], c1 = cp[B + 1 - cpo];
+      double y = 0.0, N = 1.0;
+      for (int32_t c = c0; c < c1; ++c) {
+        y += yc[c - ycs.org];
+        N += nc ? nc[c - nco] : 1.0;
+      }
+      yp[B - po] = y;
+      np[B - po] = N;
+    }
+  }
+  // ---- down
+  const double rho = scal[S_SHIFT];
+  double rz = 0.0;
+  for (int t = nl - 2; t >= 0; --t) {  // child level k = k0+t, parent level k+1
+    __syncthreads();
+    const int k = k0 + t;
+    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t + 1]);
+    const int64_t cpo = Ls.cp[t + 1].org;
+    const double* ki = seg_ptr<double>(sm, Ls.ki[t + 1]);
+    const int64_t kio = Ls.ki[t + 1].org;
+    const double* lo = seg_ptr<double>(sm, Ls.lo[t]);
+    const int64_t loo = Ls.lo[t].org;
+    const Seg& zps = (t + 1 == nl - 1) ? Ls.zt : Ls.z[t + 1];
+    const Seg& wps = (t + 1 == nl - 1) ? Ls.wt : Ls.w[t + 1];
+    const double* zp = seg_ptr<double>(sm, zps);
+    const double* wp = seg_ptr<double>(sm, wps);
+    const Seg& ycs = (t == 0) ? Ls.y0 : Ls.y[t];
+    const double* yc = seg_ptr<double>(sm, ycs);
+    const double* nc = (t == 0) ? (FIRST ? nullptr : seg_ptr<double>(sm, Ls.n0)) : seg_ptr<double>(sm, Ls.nn[t]);
+    const int64_t nco = (t == 0) ? Ls.n0.org : Ls.nn[t].org;
+    double* zc = (t == 0) ? (FIRST ? zout : Zg + lv.off[k - 1]) : seg_ptr<double>(sm, Ls.z[t]);
+    double* wc = (t == 0) ? (FIRST ? zout : Wg + lv.off[k - 1]) : seg_ptr<double>(sm, Ls.w[t]);
+    const int64_t zco = (t == 0) ? 0 : Ls.z[t].org;
+    const double ckk = lv.ck[k];
+    const bool out1 = FIRST && (t == 0);
+    for (int64_t B = sa[t + 1] + threadIdx.x; B < sb[t + 1]; B += TT) {
+      const int64_t s0 = cp[B - cpo], s1 = cp[B + 1 - cpo];
+      const int64_t lb = 3 * (-2 * B - 2) - loo;  // lo[lb + 3 p + j]
+      block_solve(
+          s0, s1, [&](int j) { return ki[3 * B + j - kio]; }, [&](int64_t p, int j) { return lo[lb + 3 * p + j]; },
+          zp[B - zps.org], lv.negmu * wp[B - wps.org],
+          [&](int64_t p) { return out1 ? yc[p - ycs.org] - rho : ckk * yc[p - ycs.org] - rho * nc[p - nco]; },
+          [&](int64_t p, double z, double w) {
+            if (out1) {
+              rz += yc[p - ycs.org] * w;
+              zc[p] = w;
+            } else {
+              zc[p - zco] = z;
+              wc[p - zco] = w;
+            }
+          });
+    }
+  }
+  pdl_trigger();
+  if (FIRST) {
+    rz = block_sum<TT>(rz);
+    if (threadIdx.x == 0) part[tile] = rz;
+    if (mode != M_APPLY && last_block(&cnt[C_DOWN])) {
+      const double tot = block_sum_partials<TT>(part, gridDim.x);
+      if (threadIdx.x == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+    }
+  }
+}
+
+// ------------------------------------------------------ per-level kernels
+// (a tier whose aggregates are too large to tile: one level, one thread per
+// aggregate)  y_{k+1} = P^T y_k
+__global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
+                                                const double* __restrict__ yin, double* __restrict__ yout,
+                                                const unsigned int* __restrict__ cnt, int mode) {
+  pdl_wait();
+  if (mode == M_ITER && cnt[C_DONE]) return;
+  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (B < lv.n[k]) {
+    const int32_t* cp = cptr + lv.cpo[k - 1];
+    double y = 0.0;
+    for (int32_t c = cp[B]; c < cp[B + 1]; ++c) y += yin[c];
+    yout[B] = y;
+  }
+}
+
+// z_k, w_k from z_{k+1}, w_{k+1}; at level 1 the output R r and (r, R r)
+template <bool LEVEL1>
+__global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
+                                                  const double* __restrict__ kinv, const double* __restrict__ lof,
+                                                  const double* __restrict__ yk, const double* __restrict__ Nsub,
+                                                  const double* __restrict__ zB, const double* __restrict__ wB,
+                                                  double* __restrict__ zk, double* __restrict__ wk,
+                                                  double* __restrict__ part, double* __restrict__ scal,
+                                                  unsigned int* __restrict__ cnt, int mode) {
+  pdl_wait();
+  if (mode != M_APPLY && cnt[C_DONE]) return;
+  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double rho = scal[S_SHIFT];
+  const double ckk = lv.ck[k];
+  double rz = 0.0;
+  if (B < lv.n[k]) {
+    const int32_t* cp = cptr + lv.cpo[k - 1];
+    const double* Nk = Nsub + lv.off[k - 1];
+    const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
+    const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
+    block_solve(
+        cp[B], cp[B + 1], [&](int j) { return ki[j]; }, [&](int64_t p, int j) { return lof[lb + 3 * p + j]; }, zB[B],
+        lv.negmu * wB[B], [&](int64_t p) { return LEVEL1 ? yk[p] - rho : ckk * yk[p] - rho * Nk[p]; },
+        [&](int64_t p, double z, double w) {
+          if (LEVEL1) { rz += yk[p] * w; wk[p] = w; }
+          else { zk[p] = z; wk[p] = w; }
+        });
+  }
+  if (LEVEL1) {
+    rz = block_sum<TPB>(rz);
+    if (threadIdx.x == 0) part[blockIdx.x] = rz;
+    if (mode != M_APPLY && last_block(&cnt[C_DOWN])) {
+      const double tot = block_sum_partials<TPB>(part, gridDim.x);
+      if (threadIdx.x == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+    }
+  }
+}
+
+// --------------------------------------------------------- coarse kernel
+// Single CTA: levels Kc..L up-sweep, the top solve, levels L..Kc down-sweep,
+// everything staged in / computed into shared memory.  When Kc == 1 it also
+// produces the level-1 output and (r, R r).
+__global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, int stage_pinv,
+                                               const int32_t* __restrict__ cptr, const double* __restrict__ kinv,
+                                               const double* __restrict__ lof, const double* __restrict__ Nsub,
+                                               const double* __restrict__ pinv_g, const double* __restrict__ y0src,
+                                               double* __restrict__ Zg, double* __restrict__ Wg,
+                                               double* __restrict__ zout, const double* __restrict__ part_gd,
+                                               int64_t npart, double* __restrict__ scal, unsigned int* __restrict__ cnt,
+                                               int mode) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ CoarseLayout C;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int sdone;
+  __shared__ double sh_rho, sh_m;
+  const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1;
+  if (threadIdx.x == 0) {
+    coarse_layout(lv, stage_pinv != 0, C);
+    mbar_init(&bar, 1);
+    uint32_t cb = C.pinv.nbytes;
+    for (int t = 1; t < nl; ++t) cb += C.cp[t].nbytes + C.ki[t].nbytes;
+    for (int t = 0; t + 1 < nl; ++t) cb += C.lo[t].nbytes;
+    for (int t = 0; t < nl; ++t) cb += C.nn[t].nbytes;
+    if (cb) mbar_expect_tx(&bar, cb);
+    for (int t = 1; t < nl; ++t) {
+      stage_issue(C.cp[t], sm, cptr, 4, &bar);
+      stage_issue(C.ki[t], sm, kinv, 8, &bar);
+    }
+    for (int t = 0; t + 1 < nl; ++t) stage_issue(C.lo[t], sm, lof, 8, &bar);
+    for (int t = 0; t < nl; ++t) stage_issue(C.nn[t], sm, Nsub, 8, &bar);
+    stage_issue(C.pinv, sm, pinv_g, 8, &bar);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+    if (!sdone && C.y0.nbytes) {
+      mbar_expect_tx(&bar, C.y0.nbytes);
+      stage_issue(C.y0, sm, y0src, 8, &bar);
+    }
+    mbar_arrive(&bar);
+  }
+  __syncthreads();
+  double gd = 0.0;
+  if (!sdone)
+    for (int64_t i = threadIdx.x; i < npart; i += CT) gd += __ldcg(part_gd + i);
+  mbar_wait(&bar, 0);
+  if (sdone) return;
+
+  auto yseg = [&](int t) -> const Seg& { return t == 0 ? C.y0 : C.y[t]; };
+  // ---- up
+  for (int t = 1; t < nl; ++t) {  // child level Kc+t-1, parent Kc+t
+    __syncthreads();
+    const int32_t* cp = seg_ptr<int32_t>(sm, C.cp[t]);
+    const int64_t cpo = C.cp[t].org;
+    const Seg& ycs = yseg(t - 1);
+    const double* yc = seg_ptr<double>(sm, ycs);
+    double* yp = seg_ptr<double>(sm, C.y[t]);
+    for (int64_t B = threadIdx.x; B < lv.n[Kc + t - 1]; B += CT) {
+      double y = 0.0;
+      for (int32_t c = cp[B - cpo]; c < cp[B + 1 - cpo]; ++c) y += yc[c - ycs.org];
+      yp[B] = y;
+    }
+  }
+  // ---- top solve
+  __syncthreads();
+  const int ntop = (int)lv.n[L - 1];
+  const Seg& yts = yseg(nl - 1);
+  const double* yt = seg_ptr<double>(sm, yts);
+  const double* Nt = seg_ptr<double>(sm, C.nn[nl - 1]);
+  const int64_t Nto = C.nn[nl - 1].org;
+  double ysum = 0.0;
+  for (int i = threadIdx.x; i < ntop; i += CT) ysum += yt[i - yts.org];
+  ysum = block_sum<CT>(ysum);
+  gd = block_sum<CT>(gd);
+  if (threadIdx.x == 0) sh_rho = lv.c_sum * ysum / lv.n_tilde;
+  __syncthreads();
+  const double rho = sh_rho;
+  double* tt = seg_ptr<double>(sm, C.tt);
+  for (int i = threadIdx.x; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i - yts.org] - rho * Nt[i - Nto];
+  __syncthreads();
+  const double* pinv = stage_pinv ? seg_ptr<double>(sm, C.pinv) - C.pinv.org : pinv_g;
+  double* zt = seg_ptr<double>(sm, C.z[nl - 1]);
+  double* wt = seg_ptr<double>(sm, C.w[nl - 1]);
+  double nz = 0.0;
+  for (int i = threadIdx.x; i < ntop; i += CT) {
+    double zi = 0.0;
+    for (int j = 0; j < ntop; ++j) zi += pinv[(int64_t)i * ntop + j] * tt[j];
+    zt[i] = zi;
+    nz += Nt[i - Nto] * zi;
+  }
+  nz = block_sum<CT>(nz);
+  if (threadIdx.x == 0) {
+    sh_m = (nz + gd - rho * lv.GN) / lv.n_tilde;
+    scal[S_SHIFT] = rho;
+  }
+  __syncthreads();
+  double rz = 0.0;
+  for (int i = threadIdx.x; i < ntop; i += CT) {
+    const double z = zt[i] - sh_m;
+    zt[i] = z;
+    wt[i] = z;
+    if (L == 1) { rz += yt[i - yts.org] * z; zout[i] = z; }
+  }
+  // ---- down
+  for (int t = nl - 2; t >= 0; --t) {  // child level k = Kc+t, parent k+1
+    __syncthreads();
+    const int k = Kc + t;
+    const int32_t* cp = seg_ptr<int32_t>(sm, C.cp[t + 1]);
+    const int64_t cpo = C.cp[t + 1].org;
+    const double* ki = seg_ptr<double>(sm, C.ki[t + 1]);
+    const int64_t kio = C.ki[t + 1].org;
+    const double* lo = seg_ptr<double>(sm, C.lo[t]);
+    const int64_t loo = C.lo[t].org;
+    const double* zp = seg_ptr<double>(sm, C.z[t + 1]);
+    const double* wp = seg_ptr<double>(sm, C.w[t + 1]);
+    const Seg& ycs = yseg(t);
+    const double* yc = seg_ptr<double>(sm, ycs);
+    const double* nc = seg_ptr<double>(sm, C.nn[t]);
+    const int64_t nco = C.nn[t].org;
+    double* zc = seg_ptr<double>(sm, C.z[t]);
+    double* wc = seg_ptr<double>(sm, C.w[t]);
+    const double ckk = lv.ck[k];
+    const bool out1 = (k == 1);
+    for (int64_t B = threadIdx.x; B < lv.n[k]; B += CT) {
+      const int64_t lb = 3 * (-2 * B - 2) - loo;
+      block_solve(
+          cp[B - cpo], cp[B + 1 - cpo], [&](int j) { return ki[3 * B + j - kio]; },
+          [&](int64_t p, int j) { return lo[lb + 3 * p + j]; }, zp[B], lv.negmu * wp[B],
+          [&](int64_t p) { return out1 ? yc[p - ycs.org] - rho : ckk * yc[p - ycs.org] - rho * nc[p - nco]; },
+          [&](int64_t p, double z, double w) {
+            if (out1) { rz += yc[p - ycs.org] * w; zout[p] = w; }
+            else { zc[p] = z; wc[p] = w; }
+          });
+    }
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (Kc > 1) {
+    const int64_t nk = lv.n[Kc - 1], base = lv.off[Kc - 1];
+    const double* zc = seg_ptr<double>(sm, C.z[0]);
+    const double* wc = seg_ptr<double>(sm, C.w[0]);
+    for (int64_t i = threadIdx.x; i < nk; i += CT) { Zg[base + i] = zc[i]; Wg[base + i] = wc[i]; }
+  } else {
+    rz = block_sum<CT>(rz);
+    if (threadIdx.x == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
+  }
+}
+
+// ------------------------------------------------------- unpreconditioned
+// R = I: r -= alpha q, rr; z = r so rz = rr -> beta  (x deferred into L p)
+__global__ void __launch_bounds__(TPB) k_update_cg(int64_t n, double* __restrict__ r, const double* __restrict__ q,
+                                                   double* __restrict__ part, double* __restrict__ scal,
+                                                   unsigned int* __restrict__ cnt, int mode) {
+  pdl_wait();
+  if (mode == M_ITER && cnt[C_DONE]) return;
+  const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
   double d = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * q[i];
-    r[i] = ri;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double ri = r[i];
+    if (mode == M_ITER) {
+      ri -= alpha * q[i];
+      r[i] = ri;
+    }
     d += ri * ri;
   }
-  const double bs = block_sum<TPB>(d);
-  if (threadIdx.x == 0) part[blockIdx.x] = bs;
+  pdl_trigger();
+  d = block_sum<TPB>(d);
+  if (threadIdx.x == 0) part[blockIdx.x] = d;
   if (last_block(&cnt[C_UPD])) {
-    const double rr = block_sum_array<TPB>(part, gridDim.x);
+    const double rr = block_sum_partials<TPB>(part, gridDim.x);
     if (threadIdx.x == 0) {
-      scal[S_RR] = rr;
-      cnt[C_IT] += 1;
-      if (rr <= scal[S_TOL2]) cnt[C_DONE] = 1;
+      finish_rr(rr, scal, cnt, mode);
+      if (!cnt[C_DONE]) finish_rz(rr, scal, mode);
       cnt[C_UPD] = 0;
     }
   }
 }
 
-// ----------------------------------------------------------- MSP up-sweep
-// Restriction by P(mu)^T fused with the forward elimination of the block tree
-// T~: for level-(k+1) node B with children S,
-//   y_B = sum_{c in S} y_c              (P^T, unscaled)
-//   s_B = (-mu)^k y_B + sum_{c in S} s_c  (subtree sum of r~ = P(mu)^T r)
-//   gdot += sum_c g_c s_c               (for the mean of z~, see k_top)
-__global__ void __launch_bounds__(TPB) k_up(int64_t nB, const int32_t* __restrict__ cptr,
-                                            const double* __restrict__ yin, const double* __restrict__ sin,
-                                            const double* __restrict__ g, double* __restrict__ yout,
-                                            double* __restrict__ sout, double negmu_k,
-                                            double* __restrict__ part, const unsigned int* __restrict__ cnt,
-                                            int check_done) {
-  if (check_done && cnt[C_DONE]) return;
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double gs = 0.0;
-  if (B < nB) {
-    const int32_t c0 = cptr[B], c1 = cptr[B + 1];
-    double y = 0.0, s = 0.0;
-    for (int32_t c = c0; c < c1; ++c) {
-      const double sc = sin[c];
-      y += yin[c];
-      s += sc;
-      gs += g[c] * sc;
-    }
-    yout[B] = y;
-    sout[B] = negmu_k * y + s;
-  }
-  const double bs = block_sum<TPB>(gs);
-  if (threadIdx.x == 0) part[blockIdx.x] = bs;
-}
-
-// ------------------------------------------------------------- top solve
-// rho = c sum(r) / n~ makes the right-hand side compatible (r~ - rho 1 is the
-// projection of r~ = P^T r off the ones vector); z_top = (sigma_l L_l)^+ s'_top;
-// then shift so that the whole z~ has zero mean (z~ = L_T~^+ r~, minimum norm):
-//   sum z~ = sum_T N_T z_T + sum_{non-top} g_i (s_i - rho N_i).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_top(int ntop, const double* __restrict__ ytop,
-                                            const double* __restrict__ stop,
-                                            const double* __restrict__ Ntop,
-                                            const double* __restrict__ pinv, const double* __restrict__ part,
-                                            int64_t npart, double c_sum, double n_tilde, double GN,
-                                            double* __restrict__ ztop, double* __restrict__ wtop,
-                                            double* __restrict__ scal, const unsigned int* __restrict__ cnt,
-                                            int check_done) {
-  if (check_done && cnt[C_DONE]) return;
-  __shared__ double t[256];
-  __shared__ double sh_rho, sh_m;
-  const double gdot = block_sum_array<NT>(part, npart);
-  double ys = 0.0;
-  for (int i = threadIdx.x; i < ntop; i += NT) ys += ytop[i];
-  ys = block_sum<NT>(ys);
-  if (threadIdx.x == 0) sh_rho = c_sum * ys / n_tilde;
-  __syncthreads();
-  const double rho = sh_rho;
-  for (int i = threadIdx.x; i < ntop; i += NT) t[i] = stop[i] - rho * Ntop[i];
-  __syncthreads();
-  double zi = 0.0, nz = 0.0;
-  if (threadIdx.x < ntop) {
-    const int i = threadIdx.x;
-    for (int j = 0; j < ntop; ++j) zi += pinv[(int64_t)i * ntop + j] * t[j];
-    nz = Ntop[i] * zi;
-  }
-  nz = block_sum<NT>(nz);
-  if (threadIdx.x == 0) {
-    sh_m = (nz + gdot - rho * GN) / n_tilde;
-    scal[S_SHIFT] = rho;
-  }
-  __syncthreads();
-  if (threadIdx.x < ntop) {
-    ztop[threadIdx.x] = zi - sh_m;
-    wtop[threadIdx.x] = zi - sh_m;
-  }
-}
-
-// ----------------------------------------------------------- MSP down-sweep
-// Back substitution of T~ fused with the prolongation P(mu) (Horner form):
-// for children S of B:  t = s_S - rho N_S,  zeta = K_S^{-1} t (pair + leftover
-// elimination with the factors of k_msp_factor),  z_c = z_B + zeta_c,
-// w_c = z_c + (-mu) w_B.  At level 1, w_c is the output R r; mode 1/2 also
-// reduce (r, z) for PCG (1: rho = rz; 2: beta = rz / rho, rho = rz).
-template <bool LEVEL1>
-__global__ void __launch_bounds__(TPB) k_down(int64_t nB, const int32_t* __restrict__ cptr,
-                                              const double* __restrict__ sin, const double* __restrict__ Nk,
-                                              const double* __restrict__ c0, const double* __restrict__ c1,
-                                              const double* __restrict__ c2, const double* __restrict__ zB,
-                                              const double* __restrict__ wB, double* __restrict__ zout,
-                                              double* __restrict__ wout, double negmu,
-                                              double* __restrict__ part, double* __restrict__ scal,
-                                              unsigned int* __restrict__ cnt, int mode) {
-  if (mode >= 2 && cnt[C_DONE]) return;
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const double rho = scal[S_SHIFT];
-  double rz = 0.0;
-  if (B < nB) {
-    const int32_t s0 = cptr[B], s1 = cptr[B + 1];
-    const double zb = zB[B], wb = negmu * wB[B];
-    const double tu = sin[s0] - rho * (LEVEL1 ? 1.0 : Nk[s0]);
-    const double tv = sin[s0 + 1] - rho * (LEVEL1 ? 1.0 : Nk[s0 + 1]);
-    double au = tu, av = tv;
-    for (int32_t p = s0 + 2; p < s1; ++p) {
-      const double tx = sin[p] - rho * (LEVEL1 ? 1.0 : Nk[p]);
-      au += c0[p] * tx;
-      av += c1[p] * tx;
-    }
-    const double kuu = c0[s0], kuv = c1[s0], kvv = c2[s0];
-    const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
-    {
-      const double z = zb + zu, ww = z + wb;
-      if (!LEVEL1) zout[s0] = z;
-      wout[s0] = ww;
-      if (LEVEL1) rz += sin[s0] * ww;
-    }
-    {
-      const double z = zb + zv, ww = z + wb;
-      if (!LEVEL1) zout[s0 + 1] = z;
-      wout[s0 + 1] = ww;
-      if (LEVEL1) rz += sin[s0 + 1] * ww;
-    }
-    for (int32_t p = s0 + 2; p < s1; ++p) {
-      const double tx = sin[p] - rho * (LEVEL1 ? 1.0 : Nk[p]);
-      const double zx = c2[p] * tx + c0[p] * zu + c1[p] * zv;
-      const double z = zb + zx, ww = z + wb;
-      if (!LEVEL1) zout[p] = z;
-      wout[p] = ww;
-      if (LEVEL1) rz += sin[p] * ww;
-    }
-  }
-  if (LEVEL1 && mode >= 1) {
-    const double bs = block_sum<TPB>(rz);
-    if (threadIdx.x == 0) part[blockIdx.x] = bs;
-    if (last_block(&cnt[C_DOWN])) {
-      const double tot = block_sum_array<TPB>(part, gridDim.x);
-      if (threadIdx.x == 0) {
-        if (mode == 2) scal[S_BETA] = tot / scal[S_RHO];
-        else scal[S_BETA] = 0.0;
-        scal[S_RHO] = tot;
-        cnt[C_DOWN] = 0;
-      }
-    }
-  }
-}
-
-// p = z + beta p
-__global__ void __launch_bounds__(TPB) k_pupdate(int64_t n, const double* __restrict__ z, double* __restrict__ p,
-                                                 const double* __restrict__ scal,
-                                                 const unsigned int* __restrict__ cnt, int check_done) {
-  if (check_done && cnt[C_DONE]) return;
-  const double beta = scal[S_BETA];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = z[i] + beta * p[i];
-}
-
-// unpreconditioned CG: z = r, rho = (r, r)
-__global__ void __launch_bounds__(TPB) k_copy_dot(int64_t n, const double* __restrict__ r, double* __restrict__ z,
-                                                  double* __restrict__ part, double* __restrict__ scal,
-                                                  unsigned int* __restrict__ cnt, int mode) {
-  if (mode >= 2 && cnt[C_DONE]) return;
-  double d = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double ri = r[i];
-    z[i] = ri;
-    d += ri * ri;
-  }
-  const double bs = block_sum<TPB>(d);
-  if (threadIdx.x == 0) part[blockIdx.x] = bs;
-  if (last_block(&cnt[C_DOWN])) {
-    const double tot = block_sum_array<TPB>(part, gridDim.x);
-    if (threadIdx.x == 0) {
-      scal[S_BETA] = (mode == 2) ? tot / scal[S_RHO] : 0.0;
-      scal[S_RHO] = tot;
-      cnt[C_DOWN] = 0;
-    }
-  }
-}
-
-__global__ void k_init_state(double* scal, unsigned int* cnt, double tol2, const double* bb) {
+__global__ void k_init_state(double* scal, unsigned int* cnt, double rtol2) {
+  pdl_wait();
   for (int i = 0; i < S_NSCAL; ++i) scal[i] = 0.0;
   for (int i = 0; i < C_NCNT; ++i) cnt[i] = 0;
-  scal[S_BB] = *bb;
-  scal[S_TOL2] = tol2 * (*bb);
-  if (*bb == 0.0) cnt[C_DONE] = 1;
+  scal[S_RTOL2] = rtol2;
 }
 
-__global__ void __launch_bounds__(TPB) k_dot_part(int64_t n, const double* __restrict__ a,
-                                                  const double* __restrict__ b, double* __restrict__ part,
-                                                  double* __restrict__ out, unsigned int* __restrict__ cnt) {
-  double d = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    d += a[i] * b[i];
-  const double bs = block_sum<TPB>(d);
-  if (threadIdx.x == 0) part[blockIdx.x] = bs;
-  if (last_block(&cnt[C_UPD])) {
-    const double tot = block_sum_array<TPB>(part, gridDim.x);
-    if (threadIdx.x == 0) { *out = tot; cnt[C_UPD] = 0; }
-  }
+// ------------------------------------------------------------- host side
+bool use_pdl() {
+  static const bool on = std::getenv("MSP_NO_PDL") == nullptr;
+  return on;
 }
 
-// dense top-only apply when the hierarchy has a single level (n <= 2, or a
-// graph that aggregates to one node): z = (L_G)^+ r, plus the PCG scalars.
-__global__ void __launch_bounds__(256) k_top_only(int nt, const double* __restrict__ pinv,
-                                                  const double* __restrict__ r, double* __restrict__ z,
-                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt,
-                                                  int mode) {
-  if (mode >= 2 && cnt[C_DONE]) return;
-  __shared__ double rs[256];
-  for (int i = threadIdx.x; i < nt; i += 256) rs[i] = r[i];
-  __syncthreads();
-  double zi = 0.0, rz = 0.0;
-  if (threadIdx.x < nt) {
-    for (int j = 0; j < nt; ++j) zi += pinv[threadIdx.x * nt + j] * rs[j];  // pinv kills the mean
-    z[threadIdx.x] = zi;
-    rz = rs[threadIdx.x] * zi;
-  }
-  rz = block_sum<256>(rz);
-  if (threadIdx.x == 0 && mode >= 1) {
-    scal[S_BETA] = (mode == 2) ? rz / scal[S_RHO] : 0.0;
-    scal[S_RHO] = rz;
-  }
-}
-
-int lanes_for(double mean_deg) {
-  if (mean_deg <= 3.0) return 2;
-  if (mean_deg <= 6.0) return 4;
-  if (mean_deg <= 12.0) return 8;
-  if (mean_deg <= 24.0) return 16;
-  return 32;
-}
-
-template <bool DOT>
-void launch_spmv(Handle& h, const double* x, double* y, cudaStream_t st) {
-  const double md = (double)h.nnz_adj / (double)h.n;
-  const int lanes = lanes_for(md);
-  const int64_t threads = h.n * lanes;
-  const unsigned g = grid_for(threads);
-  double* part = h.red.p;
-  double* scal = h.scal.p;
-  unsigned* cnt = h.counters.p;
-#define SPMV_CASE(L)                                                                              \
-  case L:                                                                                         \
-    k_spmv<L, DOT><<<g, TPB, 0, st>>>(h.n, h.rowptr1.p, h.col1.p, h.w1.p, x, y, part, scal, cnt); \
-    break;
-  switch (lanes) {
-    SPMV_CASE(2)
-    SPMV_CASE(4)
-    SPMV_CASE(8)
-    SPMV_CASE(16)
-    SPMV_CASE(32)
-  }
-#undef SPMV_CASE
-  MSP_LAUNCH_CHECK();
-  ++h.launches;
+template <typename... KArgs, typename... Args>
+void launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  MSP_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
 }
 
 // ----------------------------------------------------------- profiling
@@ -452,88 +833,161 @@ struct Prof {
   }
 };
 
-// partial-sum region of the up-sweep of level k (children at level k)
-int64_t up_part_off(const Handle& h, int k) {
-  int64_t o = 0;
-  for (int j = 1; j < k; ++j) o += grid_for(h.lv[j].n);
-  return o;
+// R r (MSP) on nested vectors.  mode APPLY: r -> z;  INIT / ITER: the PCG
+// step (ITER first updates r) with the scalars of reading R10.
+void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P) {
+  double* part_rr = h.red.p;                  // [cap/4]
+  double* part_rz = h.red.p + h.red_cap / 4;
+  double* part_gd = h.red.p + h.red_cap / 2;
+  unsigned* cnt = h.counters.p;
+  double* scal = h.scal.p;
+  const int nt = (int)h.tiers.size();
+  // ---- up
+  for (int i = 0; i < nt; ++i) {
+    auto& T = h.tiers[i];
+    P.begin();
+    if (T.generic) {
+      const int k = T.k0;
+      const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
+      launch(k_up_lvl, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin, h.Y.p + h.lv[k].off,
+             (const unsigned*)cnt, mode);
+      P.end(PC_MID_UP);
+    } else {
+      const int nl = T.k1 - T.k0 + 1;
+      if (T.k0 == 1)
+        launch(k_tile_up<true>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.k0, nl, (int)T.ntiles,
+               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, q, r, (const double*)h.Hvec.p, h.Y.p, part_rr,
+               part_gd, scal, cnt, mode);
+      else
+        launch(k_tile_up<false>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.k0, nl, (int)T.ntiles,
+               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, q, r, (const double*)h.Hvec.p, h.Y.p, part_rr,
+               part_gd, scal, cnt, mode);
+      P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
+    }
+    ++h.launches;
+  }
+  // ---- coarse
+  {
+    P.begin();
+    const double* y0 = (h.Kc == 1) ? r : h.Y.p;
+    launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.coarse_stage_pinv ? 1 : 0, (const int32_t*)h.cptr.p,
+           (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
+           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int64_t)h.tiers[0].ntiles, scal, cnt, mode);
+    P.end(PC_COARSE);
+    ++h.launches;
+  }
+  // ---- down
+  for (int i = nt - 1; i >= 0; --i) {
+    auto& T = h.tiers[i];
+    if (!T.generic && T.k1 == T.k0) continue;  // the (1,1) update-only tier
+    P.begin();
+    if (T.generic) {
+      const int k = T.k0;
+      const int64_t ok = h.lv[k - 1].off, op = h.lv[k].off;
+      if (k == 1)
+        launch(k_down_lvl<true>, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+               (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p,
+               (const double*)(h.Z.p + op), (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt,
+               mode);
+      else
+        launch(k_down_lvl<false>, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+               (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)(h.Y.p + ok),
+               (const double*)h.Nsub.p, (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok,
+               h.W.p + ok, part_rz, scal, cnt, mode);
+      P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
+    } else {
+      const int nl = T.k1 - T.k0 + 1;
+      if (T.k0 == 1)
+        launch(k_tile_down<true>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.k0, nl, (int)T.ntiles,
+               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
+               cnt, mode);
+      else
+        launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.k0, nl, (int)T.ntiles,
+               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
+               scal, cnt, mode);
+      P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
+    }
+    ++h.launches;
+  }
 }
 
-// R r for the MSP, nested numbering; mode 0: plain apply, 1: PCG init, 2: PCG iteration
-void msp_sweeps(Handle& h, const double* r, double* z, cudaStream_t st, int mode, Prof* pf = nullptr) {
-  Prof local(h, st);
-  Prof& P = pf ? *pf : local;
-  const int L = h.levels;
-  const int check = mode >= 2 ? 1 : 0;
-  double* part = h.red.p;
-  double* part_up = h.red.p + h.red_cap / 2;  // up-sweep partials live in the upper half
-  if (L == 1) {
-    k_top_only<<<1, 256, 0, st>>>((int)h.lv[0].n, h.top_pinv.p, r, z, h.scal.p, h.counters.p, mode);
-    MSP_LAUNCH_CHECK();
-    ++h.launches;
-    return;
-  }
-  for (int k = 1; k < L; ++k) {
-    const LevelHost& lk = h.lv[k - 1];
-    const LevelHost& lk1 = h.lv[k];
-    const double* yin = (k == 1) ? r : h.Y.p + lk.off;
-    const double* sin = (k == 1) ? r : h.S.p + lk.off;
-    P.begin();
-    k_up<<<grid_for(lk1.n), TPB, 0, st>>>(lk1.n, h.cptr.p + h.cptr_off[k - 1], yin, sin, h.gvec.p + lk.off,
-                                          h.Y.p + lk1.off, h.S.p + lk1.off, h.neg_mu_pow[k],
-                                          part_up + up_part_off(h, k), h.counters.p, check);
-    MSP_LAUNCH_CHECK();
-    P.end(k == 1 ? PC_UP1 : PC_UPC);
-    ++h.launches;
-  }
-  const LevelHost& lt = h.lv[L - 1];
-  const int64_t npart = up_part_off(h, L);
-  P.begin();
-  k_top<256><<<1, 256, 0, st>>>((int)lt.n, h.Y.p + lt.off, h.S.p + lt.off, h.Nsub.p + lt.off, h.top_pinv.p,
-                                part_up, npart, h.c_sum, (double)h.n_tilde, h.GN, h.Z.p + lt.off,
-                                h.W.p + lt.off, h.scal.p, h.counters.p, check);
-  MSP_LAUNCH_CHECK();
-  P.end(PC_TOP);
+template <bool PCG>
+void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
+                 cudaStream_t st) {
+  launch(k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
+         (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
+         (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
+         (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p);
   ++h.launches;
-  for (int k = L - 1; k >= 1; --k) {
-    const LevelHost& lk = h.lv[k - 1];
-    const LevelHost& lk1 = h.lv[k];
+}
+
+// one PCG iteration (reading R10): p = z + beta p, q = L p (x += alpha p
+// deferred), r -= alpha q, z = R r
+void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t st, Prof& P) {
+  double* pold = h.pparity ? h.vp2.p : h.vp.p;
+  double* pnew = h.pparity ? h.vp.p : h.vp2.p;
+  h.pparity ^= 1;
+  const double* z = (precond == MSP_PRECOND_MSP) ? h.vz.p : h.vr.p;
+  P.begin();
+  launch_spmv<true>(h, z, pold, pnew, h.vq.p, x, st);
+  P.end(PC_SPMV);
+  if (precond == MSP_PRECOND_MSP) {
+    msp_sweeps(h, lv, h.vq.p, h.vr.p, h.vz.p, st, M_ITER, P);
+  } else {
     P.begin();
-    if (k >= 2) {
-      k_down<false><<<grid_for(lk1.n), TPB, 0, st>>>(
-          lk1.n, h.cptr.p + h.cptr_off[k - 1], h.S.p + lk.off, h.Nsub.p + lk.off, h.c0.p + lk.off,
-          h.c1.p + lk.off, h.c2.p + lk.off, h.Z.p + lk1.off, h.W.p + lk1.off, h.Z.p + lk.off,
-          h.W.p + lk.off, -h.mu, part, h.scal.p, h.counters.p, mode >= 2 ? 2 : 0);
-    } else {
-      k_down<true><<<grid_for(lk1.n), TPB, 0, st>>>(
-          lk1.n, h.cptr.p + h.cptr_off[0], r, nullptr, h.c0.p, h.c1.p, h.c2.p, h.Z.p + lk1.off,
-          h.W.p + lk1.off, nullptr, z, -h.mu, part, h.scal.p, h.counters.p, mode);
-    }
-    MSP_LAUNCH_CHECK();
-    P.end(k == 1 ? PC_DOWN1 : PC_DOWNC);
+    launch(k_update_cg, std::min<unsigned>(grid_for(h.n), 148u * 8u), TPB, 0, st, h.n, h.vr.p,
+           (const double*)h.vq.p, h.red.p, h.scal.p, h.counters.p, (int)M_ITER);
+    P.end(PC_TILE_UP);
     ++h.launches;
   }
 }
 
 }  // namespace
 
+void release_graph(Handle& h) {
+  if (h.graph) cudaGraphExecDestroy(h.graph);
+  h.graph = nullptr;
+  h.graph_batch = 0;
+}
+
 void alloc_solve_workspace(Handle& h) {
   const int64_t nt = h.n_tilde;
-  h.Y.alloc(nt); h.S.alloc(nt); h.Z.alloc(nt); h.W.alloc(nt);
-  // partials: the SpMV grid is the largest per-launch grid; the up-sweep
-  // partials of all levels go to the upper half
-  const double md = (double)h.nnz_adj / (double)h.n;
-  int64_t need = grid_for(h.n * lanes_for(md));
-  need = std::max<int64_t>(need, grid_for(h.n));
-  int64_t upn = 0;
-  for (int k = 1; k < h.levels; ++k) upn += grid_for(h.lv[k].n);
-  h.red_cap = 2 * std::max<int64_t>(need, upn) + 64;
+  h.Y.alloc(nt + 8); h.Z.alloc(nt + 8); h.W.alloc(nt + 8);
+  MSP_CUDA(cudaMemset(h.Y.p, 0, (nt + 8) * sizeof(double)));
+  {
+    int dev = 0, sms = 148;
+    MSP_CUDA(cudaGetDevice(&dev));
+    MSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int per_sm = 8;
+    if (const char* e = std::getenv("MSP_SPMV_BLOCKS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+    const int64_t want = grid_for(std::max<int64_t>(h.nslices, 1) * 32);
+    h.spmv_grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * per_sm);
+  }
+  // partials: [0, cap/4) SpMV / rr, [cap/4, cap/2) rz, [cap/2, cap) gdot
+  int64_t need = std::max<int64_t>({(int64_t)h.spmv_grid, (int64_t)grid_for(h.n), 1});
+  for (auto& T : h.tiers) need = std::max<int64_t>(need, T.ntiles);
+  if (h.lv.size() > 1) need = std::max<int64_t>(need, grid_for(h.lv[1].n));
+  h.red_cap = 4 * need + 64;
   h.red.alloc(h.red_cap);
-  h.vx.alloc(h.n); h.vr.alloc(h.n); h.vp.alloc(h.n); h.vq.alloc(h.n); h.vz.alloc(h.n); h.vb.alloc(h.n);
+  MSP_CUDA(cudaMemset(h.red.p, 0, h.red_cap * sizeof(double)));
+  for (auto* v : {&h.vx, &h.vr, &h.vp, &h.vp2, &h.vq, &h.vz, &h.vb}) {
+    v->alloc(h.n + 8);
+    MSP_CUDA(cudaMemset(v->p, 0, (h.n + 8) * sizeof(double)));
+  }
   h.counters.alloc(C_NCNT);
   h.scal.alloc(S_NSCAL);
   MSP_CUDA(cudaMemset(h.counters.p, 0, C_NCNT * sizeof(unsigned)));
   MSP_CUDA(cudaMemset(h.scal.p, 0, S_NSCAL * sizeof(double)));
+  size_t up = 0, down = 0;
+  for (auto& T : h.tiers) { up = std::max(up, T.smem_up); down = std::max(down, T.smem_down); }
+  for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>})
+    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  for (auto f : {(const void*)k_tile_down<true>, (const void*)k_tile_down<false>})
+    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)h.coarse_smem));
 }
 
 void gather_to_nested(Handle& h, const double* src, double* dst, cudaStream_t st) {
@@ -549,67 +1003,92 @@ void scatter_from_nested(Handle& h, const double* src, double* dst, cudaStream_t
 }
 
 void apply_L_nested(Handle& h, const double* x, double* y, cudaStream_t st) {
-  launch_spmv<false>(h, x, y, st);
+  launch_spmv<false>(h, x, nullptr, nullptr, y, nullptr, st);
 }
 
 void apply_R_msp_nested(Handle& h, const double* r, double* z, cudaStream_t st) {
-  msp_sweeps(h, r, z, st, 0);
+  // r is read-only in APPLY mode (the tile kernels read it as y_1)
+  Prof P(h, st);
+  const Lv lv = make_level_table(h);
+  msp_sweeps(h, lv, nullptr, const_cast<double*>(r), z, st, M_APPLY, P);
 }
 
 // PCG (reading R10) on nested-numbered vectors b -> x.
-void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol, int maxit,
-                cudaStream_t st, msp_report* rep) {
+void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol, int maxit, cudaStream_t st,
+                msp_report* rep) {
   const int64_t n = h.n;
-  const unsigned gv = std::min<unsigned>(grid_for(n), 148u * 8u);
+  const Lv lv = make_level_table(h);
   cudaEvent_t e0, e1;
   MSP_CUDA(cudaEventCreate(&e0));
   MSP_CUDA(cudaEventCreate(&e1));
   const int64_t launches0 = h.launches;
   MSP_CUDA(cudaEventRecord(e0, st));
-  // x = 0, r = b, bb = (b, b)
+  // x = 0, r = b, p_old = 0, scalars; z = R r, rho = (r, z), beta = 0
   MSP_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
   MSP_CUDA(cudaMemcpyAsync(h.vr.p, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  MSP_CUDA(cudaMemsetAsync(h.counters.p, 0, C_NCNT * sizeof(unsigned), st));
-  double* bb = h.red.p + h.red_cap - 1;
-  k_dot_part<<<gv, TPB, 0, st>>>(n, b, b, h.red.p, bb, h.counters.p);
-  k_init_state<<<1, 1, 0, st>>>(h.scal.p, h.counters.p, rtol * rtol, bb);
-  h.launches += 2;
-  MSP_LAUNCH_CHECK();
-  // z = R r, rho = (r, z), p = z
-  if (precond == MSP_PRECOND_MSP) msp_sweeps(h, h.vr.p, h.vz.p, st, 1);
-  else { k_copy_dot<<<gv, TPB, 0, st>>>(n, h.vr.p, h.vz.p, h.red.p, h.scal.p, h.counters.p, 1); ++h.launches; }
-  k_pupdate<<<gv, TPB, 0, st>>>(n, h.vz.p, h.vp.p, h.scal.p, h.counters.p, 0);  // beta = 0
+  h.pparity = 0;
+  MSP_CUDA(cudaMemsetAsync(h.vp.p, 0, n * sizeof(double), st));
+  launch(k_init_state, 1u, 1u, 0, st, h.scal.p, h.counters.p, rtol * rtol);
   ++h.launches;
-  MSP_LAUNCH_CHECK();
-
-  unsigned host_cnt[C_NCNT];
-  const int check_every = h.profile ? 1 : 16;
-  Prof P(h, st);
-  int it = 0;
-  while (it < maxit) {
-    const int batch = std::min(check_every, maxit - it);
-    for (int b2 = 0; b2 < batch; ++b2) {
-      P.begin();
-      launch_spmv<true>(h, h.vp.p, h.vq.p, st);                 // q = L p, alpha
-      P.end(PC_SPMV);
-      P.begin();
-      k_update<<<gv, TPB, 0, st>>>(n, x, h.vr.p, h.vp.p, h.vq.p, h.red.p, h.scal.p, h.counters.p);
-      P.end(PC_UPDATE);
+  {
+    Prof P(h, st);
+    if (precond == MSP_PRECOND_MSP) {
+      msp_sweeps(h, lv, nullptr, h.vr.p, h.vz.p, st, M_INIT, P);
+    } else {
+      launch(k_update_cg, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, h.vr.p, (const double*)nullptr,
+             h.red.p, h.scal.p, h.counters.p, (int)M_INIT);
       ++h.launches;
-      if (precond == MSP_PRECOND_MSP) msp_sweeps(h, h.vr.p, h.vz.p, st, 2, &P);  // z = R r, beta
-      else { k_copy_dot<<<gv, TPB, 0, st>>>(n, h.vr.p, h.vz.p, h.red.p, h.scal.p, h.counters.p, 2); ++h.launches; }
-      P.begin();
-      k_pupdate<<<gv, TPB, 0, st>>>(n, h.vz.p, h.vp.p, h.scal.p, h.counters.p, 1);
-      P.end(PC_PUPD);
-      ++h.launches;
-      MSP_LAUNCH_CHECK();
     }
-    it += batch;
+  }
+  // iterations in batches; a batch is a captured CUDA graph (even length so
+  // the p / p_old ping-pong is periodic), the done flag read once per batch
+  int batch = 32;
+  if (const char* e = std::getenv("MSP_PCG_BATCH")) batch = std::max(2, std::atoi(e) & ~1);
+  const bool use_graph = !h.profile && std::getenv("MSP_NO_GRAPH") == nullptr;
+  unsigned host_cnt[C_NCNT];
+  int it = 0;
+  Prof P(h, st);
+  while (it < maxit) {
+    const int nb = std::min(batch, maxit - it);
+    if (use_graph && nb == batch) {
+      if (!h.own_stream) {
+        MSP_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
+        MSP_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+        MSP_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+      }
+      cudaStream_t gs = h.own_stream;
+      const int key = batch * 4 + precond;
+      if (h.graph && h.graph_batch != key) release_graph(h);
+      MSP_CUDA(cudaEventRecord(h.ev_fork, st));
+      MSP_CUDA(cudaStreamWaitEvent(gs, h.ev_fork, 0));
+      if (!h.graph) {
+        const int64_t l0 = h.launches;
+        cudaGraph_t g;
+        MSP_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        for (int b2 = 0; b2 < nb; ++b2) pcg_iteration(h, lv, precond, x, gs, P);
+        MSP_CUDA(cudaStreamEndCapture(gs, &g));
+        MSP_CUDA(cudaGraphInstantiate(&h.graph, g, 0));
+        cudaGraphDestroy(g);
+        h.graph_batch = key;
+        h.graph_launches = h.launches - l0;
+      } else {
+        h.launches += h.graph_launches;
+      }
+      MSP_CUDA(cudaGraphLaunch(h.graph, gs));
+      MSP_CUDA(cudaEventRecord(h.ev_join, gs));
+      MSP_CUDA(cudaStreamWaitEvent(st, h.ev_join, 0));
+    } else {
+      for (int b2 = 0; b2 < nb; ++b2) pcg_iteration(h, lv, precond, x, st, P);
+    }
+    it += nb;
     P.flush();
     MSP_CUDA(cudaMemcpyAsync(host_cnt, h.counters.p, sizeof(host_cnt), cudaMemcpyDeviceToHost, st));
     MSP_CUDA(cudaStreamSynchronize(st));
     if (host_cnt[C_DONE]) break;
   }
+  launch(k_x_final, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, x, (const double*)h.vp.p,
+         (const double*)h.vp2.p, (const double*)h.scal.p, (const unsigned*)h.counters.p);
+  ++h.launches;
   MSP_CUDA(cudaEventRecord(e1, st));
   MSP_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -621,7 +1100,6 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
     rep->iterations = (int32_t)host_cnt[C_IT];
     rep->converged = host_cnt[C_DONE] ? 1 : 0;
     rep->relres = hs[S_BB] > 0 ? std::sqrt(hs[S_RR] / hs[S_BB]) : 0.0;
-    if (hs[S_BB] == 0.0) rep->relres = 0.0;
     rep->solve_ms = ms;
     rep->kernel_launches = h.launches - launches0;
   }
