@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(HERE, "libmsp_b200.so")
+_LIBPATH = os.environ.get("MSP_LIB_OVERRIDE") or os.path.join(HERE, "libmsp_b200.so")
 
 MSP_OK = 0
 MSP_MEM_DEVICE = 0

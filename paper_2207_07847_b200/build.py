@@ -27,13 +27,17 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=None, lib=None) -> str:
+    """Compile csrc/*.cu into `lib` (default: the in-tree libmsp_b200.so);
+    `extra` adds nvcc flags (e.g. -DMSP_TRACE for phase timestamps)."""
+    lib = lib or LIB
+    extra = list(extra or []) + os.environ.get("MSP_NVCC_EXTRA", "").split()
+    if not force and lib == LIB and not extra and not needs_build():
         return LIB
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(CSRC, src.replace(".cu", ".o" if lib == LIB else ".x.o"))
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -41,9 +45,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    cmd = [NVCC, "-shared", *ARCH, "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

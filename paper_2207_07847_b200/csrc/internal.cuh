@@ -128,11 +128,13 @@ struct Handle {
     DBuf<int32_t> tstart;     // [k1-k0+1][ntiles+1]: first level-(k0+t) node of tile j
     size_t smem_up = 0, smem_down = 0;
     bool generic = false;     // one level by per-node kernels (an aggregate too large to tile)
+    TierDesc desc{};
+    DBuf<int32_t> firstk0;    // [n_k1 + 1]: first level-k0 descendant of each level-k1 node
   };
   std::vector<Tier> tiers;
   int32_t Kc = 1;
   size_t coarse_smem = 0;
-  bool coarse_stage_pinv = false;
+  CoarseDesc cdesc{};
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
 

@@ -877,6 +877,69 @@ Lv make_level_table(const Handle& h) {
   return lv;
 }
 
+namespace {
+inline int a16(int64_t b) { return (int)((b + 15) & ~(int64_t)15); }
+
+// per-tier shared-memory layout from the largest per-level tile ranges
+// cap[t] (nodes) and caplo[t] (leftovers among level-(k0+t) children);
+// the up kernel's segments come first (smem_up is their end)
+TierDesc tier_layout(int k0, int nl, int64_t ntiles, const std::vector<int64_t>& cap,
+                     const std::vector<int64_t>& caplo) {
+  TierDesc d{};
+  d.k0 = k0;
+  d.nl = nl;
+  d.ntiles = (int)ntiles;
+  int64_t cur = 0;
+  auto take = [&](int64_t bytes) { const int o = a16(cur); cur = o + bytes; return o; };
+  d.o_uf = take((cap[nl - 1] + 1 + 8) * 4);
+  d.o_uy0 = take((cap[0] + 2) * 8);
+  d.smem_up = a16(cur);
+  cur = 0;
+  for (int t = 1; t < nl; ++t) d.o_cp[t] = take((cap[t] + 1 + 8) * 4);
+  d.o_y[0] = take((cap[0] + 2) * 8);
+  for (int t = 1; t + 1 < nl; ++t) d.o_y[t] = take(cap[t] * 8);
+  for (int t = 1; t < nl; ++t) d.o_ki[t] = take((3 * cap[t] + 2) * 8);
+  for (int t = 0; t + 1 < nl; ++t) d.o_lo[t] = take((3 * caplo[t] + 2) * 8);
+  d.o_n[0] = (k0 > 1) ? take((cap[0] + 2) * 8) : 0;
+  for (int t = 1; t + 1 < nl; ++t) {
+    d.o_n[t] = take(cap[t] * 8);
+    d.o_z[t] = take(cap[t] * 8);
+    d.o_w[t] = take(cap[t] * 8);
+  }
+  d.o_z[nl - 1] = take((cap[nl - 1] + 2) * 8);
+  d.o_w[nl - 1] = take((cap[nl - 1] + 2) * 8);
+  d.smem_down = a16(cur);
+  return d;
+}
+
+CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv) {
+  CoarseDesc d{};
+  const int L = h.levels, nl = L - Kc + 1;
+  d.nl = nl;
+  d.stage_pinv = stage_pinv ? 1 : 0;
+  int64_t cur = 0;
+  auto take = [&](int64_t bytes) { const int o = a16(cur); cur = o + bytes; return o; };
+  auto nk = [&](int t) { return h.lv[Kc + t - 1].n; };
+  for (int t = 1; t < nl; ++t) {
+    d.o_cp[t] = take((nk(t) + 1 + 8) * 4);
+    d.o_ki[t] = take((3 * nk(t) + 2) * 8);
+  }
+  for (int t = 0; t + 1 < nl; ++t) d.o_lo[t] = take((3 * (nk(t) - 2 * nk(t + 1)) + 2) * 8);
+  for (int t = 0; t < nl; ++t) d.o_n[t] = take((nk(t) + 2) * 8);
+  d.o_y[0] = take((nk(0) + 2) * 8);
+  for (int t = 1; t < nl; ++t) d.o_y[t] = take(nk(t) * 8);
+  for (int t = 0; t < nl; ++t) {
+    d.o_z[t] = take(nk(t) * 8);
+    d.o_w[t] = take(nk(t) * 8);
+  }
+  const int64_t ntop = h.lv[L - 1].n;
+  d.o_pinv = stage_pinv ? take((ntop * ntop + 2) * 8) : 0;
+  d.o_tt = take(ntop * 8);
+  d.smem = a16(cur);
+  return d;
+}
+}  // namespace
+
 // Tiers and tiles of the solve schedule.
 void build_schedule(Handle& h, cudaStream_t st) {
   const int L = h.levels;
@@ -895,27 +958,20 @@ void build_schedule(Handle& h, cudaStream_t st) {
   const Lv lv = make_level_table(h);
 
   // coarse level: smallest Kc whose levels Kc..L fit the single-CTA kernel
-  h.coarse_stage_pinv = h.lv[L - 1].n <= 32;
+  const bool stage_pinv = h.lv[L - 1].n <= 32;
   {
     int Kc = L;
     int64_t tail = 0;
     for (int k = L; k >= 1; --k) {
       tail += h.lv[k - 1].n;
-      if (tail > CMAX) break;
-      Lv t = lv;
-      t.Kc = k;
-      CoarseLayout C;
-      if ((size_t)coarse_layout(t, h.coarse_stage_pinv, C) > SMEM_CAP) break;
+      if (tail > CMAX || L - k + 1 > MAXT + 8) break;
+      if ((size_t)coarse_desc(h, k, stage_pinv).smem > SMEM_CAP) break;
       Kc = k;
     }
     h.Kc = Kc;
   }
-  Lv lvc = lv;
-  lvc.Kc = h.Kc;
-  {
-    CoarseLayout C;
-    h.coarse_smem = (size_t)coarse_layout(lvc, h.coarse_stage_pinv, C);
-  }
+  h.cdesc = coarse_desc(h, h.Kc, stage_pinv);
+  h.coarse_smem = (size_t)h.cdesc.smem;
 
   // tiers over levels 1..Kc
   h.tiers.clear();
@@ -937,6 +993,9 @@ void build_schedule(Handle& h, cudaStream_t st) {
       MSP_LAUNCH_CHECK();
       MSP_CUDA(cudaStreamSynchronize(st));
       t.smem_up = 0;  // level 1 only: nothing staged
+      t.desc.k0 = 1;
+      t.desc.nl = 1;
+      t.desc.ntiles = (int)t.ntiles;
     } else {
       k_tile_bounds<<<grid_for(nt1), TPB, 0, st>>>(t.ntiles, h.lv[k1_ - 1].n, T, first_k1->p,
                                                     t.tstart.p + (int64_t)(nl - 1) * nt1);
@@ -950,14 +1009,24 @@ void build_schedule(Handle& h, cudaStream_t st) {
       std::vector<int32_t> ts((size_t)nl * nt1);
       MSP_CUDA(cudaMemcpyAsync(ts.data(), t.tstart.p, ts.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       MSP_CUDA(cudaStreamSynchronize(st));
-      int64_t a[MAXT], b[MAXT];
+      std::vector<int64_t> cap(nl, 0), caplo(nl, 0);
       for (int64_t j = 0; j < t.ntiles; ++j) {
-        for (int u = 0; u < nl; ++u) { a[u] = ts[(size_t)u * nt1 + j]; b[u] = ts[(size_t)u * nt1 + j + 1]; }
-        TileLayout D;
-        TileLayoutUp U;
-        t.smem_down = std::max(t.smem_down, (size_t)tile_layout_down(lvc, k0_, nl, a, b, D));
-        t.smem_up = std::max(t.smem_up, (size_t)tile_layout_up(lvc, k0_, nl, a, b, U));
+        for (int u = 0; u < nl; ++u) {
+          const int64_t a = ts[(size_t)u * nt1 + j], b = ts[(size_t)u * nt1 + j + 1];
+          cap[u] = std::max(cap[u], b - a);
+          if (u + 1 < nl) {
+            const int64_t a2 = ts[(size_t)(u + 1) * nt1 + j], b2 = ts[(size_t)(u + 1) * nt1 + j + 1];
+            caplo[u] = std::max(caplo[u], (b - 2 * b2) - (a - 2 * a2));
+          }
+        }
       }
+      t.desc = tier_layout(k0_, nl, t.ntiles, cap, caplo);
+      const int64_t nk1 = h.lv[k1_ - 1].n;
+      t.firstk0.alloc(nk1 + 1 + 8);
+      MSP_CUDA(cudaMemsetAsync(t.firstk0.p, 0, (nk1 + 1 + 8) * sizeof(int32_t), st));
+      MSP_CUDA(cudaMemcpyAsync(t.firstk0.p, first_k1->p, (nk1 + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      t.smem_up = t.desc.smem_up;
+      t.smem_down = t.desc.smem_down;
     }
     h.tiers.push_back(std::move(t));
   };
@@ -966,7 +1035,7 @@ void build_schedule(Handle& h, cudaStream_t st) {
   }
   while (k0 < h.Kc) {
     // first level-k0 descendants of the levels above, and the largest subtree
-    const int kmax = std::min(h.Kc, k0 + MAXT - 1);
+    const int kmax = std::min(h.Kc, k0 + MAXT - 1);  // tier depth <= MAXT levels
     std::vector<DBuf<int32_t>> first(kmax - k0 + 1);
     first[0].alloc(h.lv[k0 - 1].n + 1);
     k_iota32<<<grid_for(h.lv[k0 - 1].n + 1), TPB, 0, st>>>(h.lv[k0 - 1].n + 1, first[0].p);

@@ -37,7 +37,10 @@ namespace msp {
 namespace {
 
 constexpr int TPB = 256;      // SpMV and per-node kernels
-constexpr int TT = 256;       // tile kernels
+#ifndef MSP_TT
+#define MSP_TT 128
+#endif
+constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 constexpr int CT = 1024;      // coarse kernel (single CTA)
 
 // device scalar slots
@@ -46,6 +49,23 @@ enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S
 enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
 // sweep modes
 enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2 };
+
+// phase timestamps for kernel-structure work (build with -DMSP_TRACE; the
+// in-tree library never defines it)
+#ifdef MSP_TRACE
+__device__ unsigned long long g_trace[8][16];
+#define TRACE(tag)                                                                                  \
+  do {                                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                                      \
+      unsigned long long t_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      g_trace[TRACE_KID][tag] = t_;                                                                 \
+    }                                                                                               \
+  } while (0)
+#else
+#define TRACE(tag) do {} while (0)
+#endif
+#define TRACE_KID 0
 
 inline unsigned grid_for(int64_t n, int tpb = TPB) {
   int64_t g = (n + tpb - 1) / tpb;
@@ -60,7 +80,6 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
@@ -91,15 +110,6 @@ __device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t byte
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-}
-
-__device__ __forceinline__ void stage_issue(const Seg& s, char* sm, const void* src, int es, uint64_t* bar) {
-  if (s.nbytes > 0) tma_1d(sm + s.soff, (const char*)src + s.gstart * es, (uint32_t)s.nbytes, bar);
-}
-
-template <typename T>
-__device__ __forceinline__ T* seg_ptr(char* sm, const Seg& s) {
-  return reinterpret_cast<T*>(sm + s.soff);
 }
 
 // ------------------------------------------------------------ reductions
@@ -154,21 +164,26 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
 // s0+1, leftovers s0+2..), K(j) the packed K'^{-1} (uu, uv, vv), C(p, j) the
 // leftover coefficients (sigma w_xu / d, sigma w_xv / d, 1 / d):
 // zeta = K_S^{-1} t, emitted as ef(p, z_B + zeta_p, z_B + zeta_p + wbm).
-template <typename TF, typename KF, typename CF, typename EF>
-__device__ __forceinline__ void block_solve(int64_t s0, int64_t s1, KF K, CF C, double zb, double wbm, TF tf,
-                                            EF ef) {
+template <typename I, typename TF, typename KF, typename CF, typename EF>
+__device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, double wbm, TF tf, EF ef) {
+  const double kuu = K(0), kuv = K(1), kvv = K(2);
   const double tu = tf(s0), tv = tf(s0 + 1);
+  if (s1 == s0 + 2) {  // a matched pair without leftovers (the common case)
+    const double zu = kuu * tu + kuv * tv, zv = kuv * tu + kvv * tv;
+    { const double z = zb + zu; ef(s0, z, z + wbm); }
+    { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
+    return;
+  }
   double au = tu, av = tv;
-  for (int64_t p = s0 + 2; p < s1; ++p) {
+  for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     au += C(p, 0) * tx;
     av += C(p, 1) * tx;
   }
-  const double kuu = K(0), kuv = K(1), kvv = K(2);
   const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
   { const double z = zb + zu; ef(s0, z, z + wbm); }
   { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
-  for (int64_t p = s0 + 2; p < s1; ++p) {
+  for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     const double zx = C(p, 2) * tx + C(p, 0) * zu + C(p, 1) * zv;
     const double z = zb + zx;
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(TPB) k_spmv(int64_t n, int64_t nslices, const 
     const bool valid = r < n;
     const bool lng = (smask[s] >> lane) & 1u;
     const int64_t base = sptr[s];
-    const int64_t width = (sptr[s + 1] - base) >> 5;
+    const int width = (int)((sptr[s + 1] - base) >> 5);
     double pi = 0.0, po = 0.0;
     if (valid) {
       if (PCG) { po = pold[r]; pi = z[r] + beta * po; }
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(TPB) k_spmv(int64_t n, int64_t nslices, const 
     }
     double acc = 0.0;
 #pragma unroll 4
-    for (int64_t k = 0; k < width; ++k) {
+    for (int k = 0; k < width; ++k) {
       const int64_t idx = base + k * 32 + lane;
       const int32_t j = scol[idx];
       const double pj = PCG ? z[j] + beta * pold[j] : z[j];
@@ -307,57 +322,71 @@ __global__ void k_x_final(int64_t n, double* __restrict__ x, const double* __res
     x[i] += alpha * p[i];
 }
 
+// ------------------------------------------------------------ tile staging
+// Stage [lo, hi) of a global array (absolute element indices, element size
+// es = 4 or 8) into shared memory at dst with one TMA bulk copy; the window
+// starts at the 16-byte-aligned element at or below lo.  Returns the skew
+// lo - window start (elements).  Called by one thread per segment; the
+// barrier's single arrival comes after every segment's expect_tx.
+__device__ __forceinline__ int stage_window(uint64_t* bar, char* dst, const void* src, int es, int64_t lo,
+                                            int64_t hi) {
+  const int64_t m = (es == 4) ? 3 : 1;
+  const int64_t a0 = lo & ~m;
+  if (hi > lo) {
+    const int64_t e0 = (hi + m) & ~m;
+    const uint32_t bytes = (uint32_t)((e0 - a0) * es);
+    mbar_expect_tx(bar, bytes);
+    tma_1d(dst, (const char*)src + a0 * es, bytes, bar);
+  }
+  return (int)(lo - a0);
+}
+
 // ------------------------------------------------------------ tile up-sweep
-// Tier k0..k1 (nl = k1-k0+1 levels), one CTA per tile.  FIRST (k0 == 1):
-// level 1 is the PCG update r -= alpha q (mode ITER) with (r, r) and
-// gdot = (r, H); otherwise y_k0 is staged from Y.  Levels k0+1..k1:
-// y = P^T y in shared memory; y_k1 to global Y.
+// Tier k0..k1, one CTA per tile.  FIRST (k0 == 1): level 1 is the PCG update
+// r -= alpha q (mode ITER) with (r, r) and gdot = (r, H); otherwise y_k0 is
+// staged from Y.  y_k1 = (P^T)^{k1-k0} y_k0 is formed directly, each level-k1
+// node summing its contiguous range of level-k0 descendants (one warp per
+// node), and written to global Y.
 template <bool FIRST>
-__global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, int k0, int nl, int ntiles,
-                                                const int32_t* __restrict__ tstart, const int32_t* __restrict__ cptr,
+__global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
+                                                const int32_t* __restrict__ tstart, const int32_t* __restrict__ firstk0,
                                                 const double* __restrict__ q, double* __restrict__ r,
                                                 const double* __restrict__ H, double* __restrict__ Yg,
                                                 double* __restrict__ part_rr, double* __restrict__ part_gd,
                                                 double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
   extern __shared__ __align__(16) char sm[];
-  __shared__ TileLayoutUp Ls;
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int64_t sa[MAXT], sb[MAXT];
-  __shared__ int sdone;
-  const int tile = blockIdx.x, nt1 = ntiles + 1;
-  if (threadIdx.x < nl) {
-    sa[threadIdx.x] = tstart[threadIdx.x * nt1 + tile];
-    sb[threadIdx.x] = tstart[threadIdx.x * nt1 + tile + 1];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tile_layout_up(lv, k0, nl, sa, sb, Ls);
+  __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone;
+  const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
     mbar_init(&bar, 1);
-    uint32_t cb = 0;
-    for (int t = 1; t < nl; ++t) cb += Ls.cp[t].nbytes;
-    if (cb) mbar_expect_tx(&bar, cb);
-    for (int t = 1; t < nl; ++t) stage_issue(Ls.cp[t], sm, cptr, 4, &bar);
+    sa0 = tstart[tile];
+    sn0 = tstart[tile + 1] - sa0;
+    if (nl > 1) {
+      sa1 = tstart[(nl - 1) * nt1 + tile];
+      sn1 = tstart[(nl - 1) * nt1 + tile + 1] - sa1;
+      skf = stage_window(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
+    }
   }
   pdl_wait();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     sdone = (mode == M_ITER) ? (int)cnt[C_DONE] : 0;
-    if (!FIRST && !sdone && Ls.y0.nbytes) {
-      mbar_expect_tx(&bar, Ls.y0.nbytes);
-      stage_issue(Ls.y0, sm, Yg, 8, &bar);
+    if (!FIRST && !sdone) {
+      const int64_t base = lv.off[k0 - 1];
+      sky0 = stage_window(&bar, sm + td.o_uy0, Yg, 8, base + sa0, base + sa0 + sn0);
     }
     mbar_arrive(&bar);
   }
   __syncthreads();
-  mbar_wait(&bar, 0);
-  if (sdone) return;
-
+  const int done = sdone;
   double rr = 0.0, gd = 0.0;
-  if (FIRST) {
+  double* y0 = reinterpret_cast<double*>(sm + td.o_uy0);
+  if (FIRST && !done) {  // level-1 update, overlapping the TMA of the descendant offsets
     const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
-    const int64_t a1 = sa[0], n1 = sb[0] - sa[0];
-    double* y0 = seg_ptr<double>(sm, Ls.y0);
-    for (int64_t i = threadIdx.x; i < n1; i += TT) {
-      const int64_t gi = a1 + i;
+    const int a1 = sa0, n1 = sn0;
+    for (int i = tid; i < n1; i += TT) {
+      const int gi = a1 + i;
       double ri = r[gi];
       if (mode == M_ITER) {
         ri -= alpha * q[gi];
@@ -368,30 +397,30 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, i
       if (nl > 1) y0[i] = ri;
     }
   }
-  for (int t = 1; t < nl; ++t) {  // child level k0+t-1, parent level k0+t
+  mbar_wait(&bar, 0);
+  if (done) return;
+  if (nl > 1) {
     __syncthreads();
-    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t]);
-    const int64_t cpo = Ls.cp[t].org;
-    const double* yc = seg_ptr<double>(sm, t == 1 ? Ls.y0 : Ls.y[t - 1]);
-    const int64_t yco = (t == 1) ? Ls.y0.org : Ls.y[t - 1].org;
-    const bool last = (t == nl - 1);
-    double* yp = last ? Yg + lv.off[k0 + t - 1] : seg_ptr<double>(sm, Ls.y[t]);
-    const int64_t ypo = last ? 0 : Ls.y[t].org;
-    for (int64_t B = sa[t] + threadIdx.x; B < sb[t]; B += TT) {
-      const int32_t c0 = cp[B - cpo], c1 = cp[B + 1 - cpo];
+    const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
+    const double* yc = y0 + (FIRST ? 0 : sky0);
+    const int a0 = sa0, np = sn1;
+    double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
+    for (int i = warp; i < np; i += TT / 32) {
+      const int c0 = f[i] - a0, c1 = f[i + 1] - a0;
       double y = 0.0;
-      for (int32_t c = c0; c < c1; ++c) y += yc[c - yco];
-      yp[B - ypo] = y;
+      for (int c = c0 + lane; c < c1; c += 32) y += yc[c];
+      y = warp_sum(y);
+      if (lane == 0) yp[i] = y;
     }
   }
   pdl_trigger();
   if (FIRST) {
     rr = block_sum<TT>(rr);
     gd = block_sum<TT>(gd);
-    if (threadIdx.x == 0) { part_rr[tile] = rr; part_gd[tile] = gd; }
+    if (tid == 0) { part_rr[tile] = rr; part_gd[tile] = gd; }
     if (mode != M_APPLY && last_block(&cnt[C_UPD])) {
       const double tot = block_sum_partials<TT>(part_rr, gridDim.x);
-      if (threadIdx.x == 0) {
+      if (tid == 0) {
         finish_rr(tot, scal, cnt, mode);
         cnt[C_UPD] = 0;
       }
@@ -403,8 +432,10 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, i
 // Tier k0..k1: recompute y (and subtree sizes N) of levels k0+1..k1-1 from
 // y_k0, read z, w at level k1, solve / prolong down to level k0.  FIRST: the
 // output R r and the partial (r, R r); otherwise z, w at level k0 to global.
+#undef TRACE_KID
+#define TRACE_KID (FIRST ? 2 : 3)
 template <bool FIRST>
-__global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv, int k0, int nl, int ntiles,
+__global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
                                                   const int32_t* __restrict__ tstart, const int32_t* __restrict__ cptr,
                                                   const double* __restrict__ kinv, const double* __restrict__ lof,
                                                   const double* __restrict__ Nsub, const double* __restrict__ y0src,
@@ -412,123 +443,165 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
                                                   double* __restrict__ zout, double* __restrict__ part,
                                                   double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
   extern __shared__ __align__(16) char sm[];
-  __shared__ TileLayout Ls;
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int64_t sa[MAXT], sb[MAXT];
-  __shared__ int sdone;
-  const int tile = blockIdx.x, nt1 = ntiles + 1;
-  if (threadIdx.x < nl) {
-    sa[threadIdx.x] = tstart[threadIdx.x * nt1 + tile];
-    sb[threadIdx.x] = tstart[threadIdx.x * nt1 + tile + 1];
+  __shared__ int sa[MAXT], sn[MAXT], skc[MAXT], skk[MAXT], skl[MAXT];
+  __shared__ int sky0, skn0, skz, skw, sdone;
+  const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  const int tid = threadIdx.x;
+  const int64_t n1 = lv.n[0];
+  TRACE(0);
+  if (tid == 0) mbar_init(&bar, 1);
+  if (tid < nl) {
+    const int a = tstart[tid * nt1 + tile];
+    sa[tid] = a;
+    sn[tid] = tstart[tid * nt1 + tile + 1] - a;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    tile_layout_down(lv, k0, nl, sa, sb, Ls);
-    mbar_init(&bar, 1);
-    uint32_t cb = Ls.n0.nbytes;
-    for (int t = 1; t < nl; ++t) cb += Ls.cp[t].nbytes + Ls.ki[t].nbytes;
-    for (int t = 0; t + 1 < nl; ++t) cb += Ls.lo[t].nbytes;
-    if (cb) mbar_expect_tx(&bar, cb);
-    for (int t = 1; t < nl; ++t) {
-      stage_issue(Ls.cp[t], sm, cptr, 4, &bar);
-      stage_issue(Ls.ki[t], sm, kinv, 8, &bar);
-    }
-    for (int t = 0; t + 1 < nl; ++t) stage_issue(Ls.lo[t], sm, lof, 8, &bar);
-    if (!FIRST) stage_issue(Ls.n0, sm, Nsub, 8, &bar);
+  // segments, one per thread, spread over the warps (g = lane * 8 + warp):
+  // [0, nl-1) child pointers, [nl-1, 2nl-2) factors, [2nl-2, 3nl-3) leftover
+  // coefficients, 3nl-3 N_k0; after the grid dependency: y_k0, z, w
+  const int g = (tid & 31) * (TT / 32) + (tid >> 5);
+  const int m1 = nl - 1;
+  if (g < m1) {
+    const int t = g + 1;
+    const int64_t base = lv.cpo[k0 + t - 2];
+    skc[t] = stage_window(&bar, sm + td.o_cp[t], cptr, 4, base + sa[t], base + sa[t] + sn[t] + 1);
+  } else if (g < 2 * m1) {
+    const int t = g - m1 + 1;
+    const int64_t base = 3 * (lv.off[k0 + t - 1] - n1 + sa[t]);
+    skk[t] = stage_window(&bar, sm + td.o_ki[t], kinv, 8, base, base + 3 * (int64_t)sn[t]);
+  } else if (g < 3 * m1) {
+    const int t = g - 2 * m1;
+    const int64_t lo0 = (int64_t)sa[t] - 2 * (int64_t)sa[t + 1];
+    const int64_t lo1 = (int64_t)(sa[t] + sn[t]) - 2 * (int64_t)(sa[t + 1] + sn[t + 1]);
+    const int64_t base = 3 * lv.lo[k0 + t - 1];
+    skl[t] = stage_window(&bar, sm + td.o_lo[t], lof, 8, base + 3 * lo0, base + 3 * lo1);
+  } else if (!FIRST && g == 3 * m1) {
+    const int64_t base = lv.off[k0 - 1];
+    skn0 = stage_window(&bar, sm + td.o_n[0], Nsub, 8, base + sa[0], base + sa[0] + sn[0]);
   }
+  TRACE(1);
   pdl_wait();
-  if (threadIdx.x == 0) {
-    sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
-    if (!sdone) {
-      const uint32_t db = Ls.y0.nbytes + Ls.zt.nbytes + Ls.wt.nbytes;
-      if (db) mbar_expect_tx(&bar, db);
-      stage_issue(Ls.y0, sm, y0src, 8, &bar);
-      stage_issue(Ls.zt, sm, Zg, 8, &bar);
-      stage_issue(Ls.wt, sm, Wg, 8, &bar);
+  TRACE(2);
+  if (tid == 0) sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+  __syncthreads();
+  const int done = sdone;
+  if (!done) {  // dynamic segments: y_k0, z and w at level k1
+    if (g == 3 * m1 + 1) {
+      const int64_t base = FIRST ? 0 : lv.off[k0 - 1];
+      sky0 = stage_window(&bar, sm + td.o_y[0], y0src, 8, base + sa[0], base + sa[0] + sn[0]);
+    } else if (g == 3 * m1 + 2 || g == 3 * m1 + 3) {
+      const bool isz = (g == 3 * m1 + 2);
+      const int64_t base = lv.off[k0 + nl - 2] + sa[nl - 1];
+      const int v = stage_window(&bar, sm + (isz ? td.o_z[nl - 1] : td.o_w[nl - 1]), isz ? Zg : Wg, 8, base,
+                                 base + sn[nl - 1]);
+      if (isz) skz = v; else skw = v;
     }
-    mbar_arrive(&bar);
   }
   __syncthreads();
+  if (tid == 0) mbar_arrive(&bar);
   mbar_wait(&bar, 0);
-  if (sdone) return;
+  TRACE(3);
+  if (done) return;
 
+  auto ylev = [&](int t) -> double* {
+    return reinterpret_cast<double*>(sm + td.o_y[t]) + (t == 0 ? sky0 : 0);
+  };
+  auto nlev = [&](int t) -> double* {
+    return reinterpret_cast<double*>(sm + td.o_n[t]) + (t == 0 ? skn0 : 0);
+  };
   // ---- recompute y and N of levels k0+1 .. k1-1
   for (int t = 1; t + 1 < nl; ++t) {
     __syncthreads();
-    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t]);
-    const int64_t cpo = Ls.cp[t].org;
-    const Seg& ycs = (t == 1) ? Ls.y0 : Ls.y[t - 1];
-    const double* yc = seg_ptr<double>(sm, ycs);
-    const double* nc = (t == 1) ? (FIRST ? nullptr : seg_ptr<double>(sm, Ls.n0)) : seg_ptr<double>(sm, Ls.nn[t - 1]);
-    const int64_t nco = (t == 1) ? Ls.n0.org : Ls.nn[t - 1].org;
-    double* yp = seg_ptr<double>(sm, Ls.y[t]);
-    double* np = seg_ptr<double>(sm, Ls.nn[t]);
-    const int64_t po = Ls.y[t].org;
-    for (int64_t B = sa[t] + threadIdx.x; B < sb[t]; B += TT) {
-      const int32_t c0 = cp[B - cpo], c1 = cp[B + 1 - cpo];
+    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[t]) + skc[t];
+    const double* yc = ylev(t - 1);
+    const double* nc = (t == 1 && FIRST) ? nullptr : nlev(t - 1);
+    double* yp = ylev(t);
+    double* np = nlev(t);
+    const int ac = sa[t - 1], npar = sn[t];
+    for (int i = tid; i < npar; i += TT) {
+      const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
       double y = 0.0, N = 1.0;
-      for (int32_t c = c0; c < c1; ++c) {
-        y += yc[c - ycs.org];
-        N += nc ? nc[c - nco] : 1.0;
+      for (int c = c0; c < c1; ++c) {
+        y += yc[c];
+        N += nc ? nc[c] : 1.0;
       }
-      yp[B - po] = y;
-      np[B - po] = N;
+      yp[i] = y;
+      np[i] = N;
     }
   }
-  // ---- down
+  TRACE(4);
+  // ---- down: levels k1-1 .. k0+1 in shared memory, then level k0 out
   const double rho = scal[S_SHIFT];
+  const double negmu = lv.negmu;
   double rz = 0.0;
-  for (int t = nl - 2; t >= 0; --t) {  // child level k = k0+t, parent level k+1
+  for (int t = nl - 2; t >= 1; --t) {  // child level k = k0+t, parent level k+1
     __syncthreads();
-    const int k = k0 + t;
-    const int32_t* cp = seg_ptr<int32_t>(sm, Ls.cp[t + 1]);
-    const int64_t cpo = Ls.cp[t + 1].org;
-    const double* ki = seg_ptr<double>(sm, Ls.ki[t + 1]);
-    const int64_t kio = Ls.ki[t + 1].org;
-    const double* lo = seg_ptr<double>(sm, Ls.lo[t]);
-    const int64_t loo = Ls.lo[t].org;
-    const Seg& zps = (t + 1 == nl - 1) ? Ls.zt : Ls.z[t + 1];
-    const Seg& wps = (t + 1 == nl - 1) ? Ls.wt : Ls.w[t + 1];
-    const double* zp = seg_ptr<double>(sm, zps);
-    const double* wp = seg_ptr<double>(sm, wps);
-    const Seg& ycs = (t == 0) ? Ls.y0 : Ls.y[t];
-    const double* yc = seg_ptr<double>(sm, ycs);
-    const double* nc = (t == 0) ? (FIRST ? nullptr : seg_ptr<double>(sm, Ls.n0)) : seg_ptr<double>(sm, Ls.nn[t]);
-    const int64_t nco = (t == 0) ? Ls.n0.org : Ls.nn[t].org;
-    double* zc = (t == 0) ? (FIRST ? zout : Zg + lv.off[k - 1]) : seg_ptr<double>(sm, Ls.z[t]);
-    double* wc = (t == 0) ? (FIRST ? zout : Wg + lv.off[k - 1]) : seg_ptr<double>(sm, Ls.w[t]);
-    const int64_t zco = (t == 0) ? 0 : Ls.z[t].org;
-    const double ckk = lv.ck[k];
-    const bool out1 = FIRST && (t == 0);
-    for (int64_t B = sa[t + 1] + threadIdx.x; B < sb[t + 1]; B += TT) {
-      const int64_t s0 = cp[B - cpo], s1 = cp[B + 1 - cpo];
-      const int64_t lb = 3 * (-2 * B - 2) - loo;  // lo[lb + 3 p + j]
+    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[t + 1]) + skc[t + 1];
+    const double* ki = reinterpret_cast<const double*>(sm + td.o_ki[t + 1]) + skk[t + 1];
+    const double* lo = reinterpret_cast<const double*>(sm + td.o_lo[t]) + skl[t];
+    const bool top = (t + 1 == nl - 1);
+    const double* zp = reinterpret_cast<const double*>(sm + td.o_z[t + 1]) + (top ? skz : 0);
+    const double* wp = reinterpret_cast<const double*>(sm + td.o_w[t + 1]) + (top ? skw : 0);
+    const double* yc = reinterpret_cast<const double*>(sm + td.o_y[t]);
+    const double* nc = reinterpret_cast<const double*>(sm + td.o_n[t]);
+    double* zc = reinterpret_cast<double*>(sm + td.o_z[t]);
+    double* wc = reinterpret_cast<double*>(sm + td.o_w[t]);
+    const int ac = sa[t], npar = sn[t + 1];
+    const double ckk = lv.ck[k0 + t];
+    for (int i = tid; i < npar; i += TT) {
+      const int lb = -3 * (2 * i + 2);
       block_solve(
-          s0, s1, [&](int j) { return ki[3 * B + j - kio]; }, [&](int64_t p, int j) { return lo[lb + 3 * p + j]; },
-          zp[B - zps.org], lv.negmu * wp[B - wps.org],
-          [&](int64_t p) { return out1 ? yc[p - ycs.org] - rho : ckk * yc[p - ycs.org] - rho * nc[p - nco]; },
-          [&](int64_t p, double z, double w) {
-            if (out1) {
-              rz += yc[p - ycs.org] * w;
-              zc[p] = w;
-            } else {
-              zc[p - zco] = z;
-              wc[p - zco] = w;
-            }
-          });
+          cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
+          [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
+          [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+          [&](int p, double z, double w) { zc[p] = z; wc[p] = w; });
     }
   }
+  {
+    __syncthreads();
+    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[1]) + skc[1];
+    const double* ki = reinterpret_cast<const double*>(sm + td.o_ki[1]) + skk[1];
+    const double* lo = reinterpret_cast<const double*>(sm + td.o_lo[0]) + skl[0];
+    const bool top = (nl == 2);
+    const double* zp = reinterpret_cast<const double*>(sm + td.o_z[1]) + (top ? skz : 0);
+    const double* wp = reinterpret_cast<const double*>(sm + td.o_w[1]) + (top ? skw : 0);
+    const double* yc = reinterpret_cast<const double*>(sm + td.o_y[0]) + sky0;
+    const double* nc = reinterpret_cast<const double*>(sm + td.o_n[0]) + skn0;
+    const int ac = sa[0], npar = sn[1];
+    const double ckk = lv.ck[k0];
+    double* zg = FIRST ? zout + ac : Zg + lv.off[k0 - 1] + ac;
+    double* wg = Wg + lv.off[k0 - 1] + ac;
+    for (int i = tid; i < npar; i += TT) {
+      const int lb = -3 * (2 * i + 2);
+      if (FIRST)
+        block_solve(
+            cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
+            [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
+            [&](int p) { return yc[p] - rho; },
+            [&](int p, double z, double w) { rz += yc[p] * w; zg[p] = w; });
+      else
+        block_solve(
+            cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
+            [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
+            [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zg[p] = z; wg[p] = w; });
+    }
+  }
+  TRACE(5);
   pdl_trigger();
   if (FIRST) {
     rz = block_sum<TT>(rz);
-    if (threadIdx.x == 0) part[tile] = rz;
+    if (tid == 0) part[tile] = rz;
     if (mode != M_APPLY && last_block(&cnt[C_DOWN])) {
       const double tot = block_sum_partials<TT>(part, gridDim.x);
-      if (threadIdx.x == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+      if (tid == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
     }
   }
 }
 
+#undef TRACE_KID
+#define TRACE_KID 0
 // ------------------------------------------------------ per-level kernels
 // (a tier whose aggregates are too large to tile: one level, one thread per
 // aggregate)  y_{k+1} = P^T y_k
@@ -586,151 +659,169 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
 
 // --------------------------------------------------------- coarse kernel
 // Single CTA: levels Kc..L up-sweep, the top solve, levels L..Kc down-sweep,
-// everything staged in / computed into shared memory.  When Kc == 1 it also
-// produces the level-1 output and (r, R r).
-__global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, int stage_pinv,
+// everything staged in / computed into shared memory (layout: CoarseDesc).
+// When Kc == 1 it also produces the level-1 output and (r, R r).
+#undef TRACE_KID
+#define TRACE_KID 1
+__global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, const __grid_constant__ CoarseDesc cd,
                                                const int32_t* __restrict__ cptr, const double* __restrict__ kinv,
                                                const double* __restrict__ lof, const double* __restrict__ Nsub,
                                                const double* __restrict__ pinv_g, const double* __restrict__ y0src,
                                                double* __restrict__ Zg, double* __restrict__ Wg,
                                                double* __restrict__ zout, const double* __restrict__ part_gd,
-                                               int64_t npart, double* __restrict__ scal, unsigned int* __restrict__ cnt,
+                                               int npart, double* __restrict__ scal, unsigned int* __restrict__ cnt,
                                                int mode) {
   extern __shared__ __align__(16) char sm[];
-  __shared__ CoarseLayout C;
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int sdone;
+  __shared__ int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
+  __shared__ int sky0, skp, sdone;
   __shared__ double sh_rho, sh_m;
-  const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1;
-  if (threadIdx.x == 0) {
-    coarse_layout(lv, stage_pinv != 0, C);
-    mbar_init(&bar, 1);
-    uint32_t cb = C.pinv.nbytes;
-    for (int t = 1; t < nl; ++t) cb += C.cp[t].nbytes + C.ki[t].nbytes;
-    for (int t = 0; t + 1 < nl; ++t) cb += C.lo[t].nbytes;
-    for (int t = 0; t < nl; ++t) cb += C.nn[t].nbytes;
-    if (cb) mbar_expect_tx(&bar, cb);
-    for (int t = 1; t < nl; ++t) {
-      stage_issue(C.cp[t], sm, cptr, 4, &bar);
-      stage_issue(C.ki[t], sm, kinv, 8, &bar);
-    }
-    for (int t = 0; t + 1 < nl; ++t) stage_issue(C.lo[t], sm, lof, 8, &bar);
-    for (int t = 0; t < nl; ++t) stage_issue(C.nn[t], sm, Nsub, 8, &bar);
-    stage_issue(C.pinv, sm, pinv_g, 8, &bar);
+  const int L = lv.L, Kc = lv.Kc, nl = cd.nl, tid = threadIdx.x;
+  const int64_t n1 = lv.n[0];
+  TRACE(0);
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  // segments, one per warp (g = lane * 32 + warp): [0, nl-1) child pointers,
+  // [nl-1, 2nl-2) factors, [2nl-2, 3nl-3) leftover coefficients,
+  // [3nl-3, 4nl-3) subtree sizes, 4nl-3 the top pseudo-inverse; after the
+  // grid dependency 4nl-2: y_Kc
+  const int g = (tid & 31) * (CT / 32) + (tid >> 5);
+  const int m1 = nl - 1;
+  if (g < m1) {
+    const int t = g + 1;
+    const int64_t base = lv.cpo[Kc + t - 2];
+    skc[t] = stage_window(&bar, sm + cd.o_cp[t], cptr, 4, base, base + lv.n[Kc + t - 1] + 1);
+  } else if (g < 2 * m1) {
+    const int t = g - m1 + 1;
+    const int64_t base = 3 * (lv.off[Kc + t - 1] - n1);
+    skk[t] = stage_window(&bar, sm + cd.o_ki[t], kinv, 8, base, base + 3 * lv.n[Kc + t - 1]);
+  } else if (g < 3 * m1) {
+    const int t = g - 2 * m1;
+    const int64_t base = 3 * lv.lo[Kc + t - 1];
+    skl[t] = stage_window(&bar, sm + cd.o_lo[t], lof, 8, base, base + 3 * (lv.n[Kc + t - 1] - 2 * lv.n[Kc + t]));
+  } else if (g < 3 * m1 + nl) {
+    const int t = g - 3 * m1;
+    const int64_t base = lv.off[Kc + t - 1];
+    skn[t] = stage_window(&bar, sm + cd.o_n[t], Nsub, 8, base, base + lv.n[Kc + t - 1]);
+  } else if (g == 3 * m1 + nl && cd.stage_pinv) {
+    const int64_t nt = lv.n[L - 1];
+    skp = stage_window(&bar, sm + cd.o_pinv, pinv_g, 8, 0, nt * nt);
   }
+  TRACE(1);
   pdl_wait();
-  if (threadIdx.x == 0) {
-    sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
-    if (!sdone && C.y0.nbytes) {
-      mbar_expect_tx(&bar, C.y0.nbytes);
-      stage_issue(C.y0, sm, y0src, 8, &bar);
-    }
-    mbar_arrive(&bar);
+  TRACE(2);
+  if (tid == 0) sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+  __syncthreads();
+  const int done = sdone;
+  if (g == 3 * m1 + nl + 1 && !done) {
+    const int64_t base = (Kc == 1) ? 0 : lv.off[Kc - 1];
+    sky0 = stage_window(&bar, sm + cd.o_y[0], y0src, 8, base, base + lv.n[Kc - 1]);
   }
   __syncthreads();
+  if (tid == 0) mbar_arrive(&bar);
   double gd = 0.0;
-  if (!sdone)
-    for (int64_t i = threadIdx.x; i < npart; i += CT) gd += __ldcg(part_gd + i);
+  if (!done)
+    for (int i = tid; i < npart; i += CT) gd += __ldcg(part_gd + i);
   mbar_wait(&bar, 0);
-  if (sdone) return;
+  TRACE(3);
+  if (done) return;
 
-  auto yseg = [&](int t) -> const Seg& { return t == 0 ? C.y0 : C.y[t]; };
+  auto yl = [&](int t) -> double* { return reinterpret_cast<double*>(sm + cd.o_y[t]) + (t == 0 ? sky0 : 0); };
+  auto nlv = [&](int t) -> const double* { return reinterpret_cast<const double*>(sm + cd.o_n[t]) + skn[t]; };
   // ---- up
   for (int t = 1; t < nl; ++t) {  // child level Kc+t-1, parent Kc+t
     __syncthreads();
-    const int32_t* cp = seg_ptr<int32_t>(sm, C.cp[t]);
-    const int64_t cpo = C.cp[t].org;
-    const Seg& ycs = yseg(t - 1);
-    const double* yc = seg_ptr<double>(sm, ycs);
-    double* yp = seg_ptr<double>(sm, C.y[t]);
-    for (int64_t B = threadIdx.x; B < lv.n[Kc + t - 1]; B += CT) {
+    const int* cp = reinterpret_cast<const int*>(sm + cd.o_cp[t]) + skc[t];
+    const double* yc = yl(t - 1);
+    double* yp = yl(t);
+    const int np = (int)lv.n[Kc + t - 1];
+    for (int i = tid; i < np; i += CT) {
       double y = 0.0;
-      for (int32_t c = cp[B - cpo]; c < cp[B + 1 - cpo]; ++c) y += yc[c - ycs.org];
-      yp[B] = y;
+      const int c1 = cp[i + 1];
+      for (int c = cp[i]; c < c1; ++c) y += yc[c];
+      yp[i] = y;
     }
   }
   // ---- top solve
   __syncthreads();
+  TRACE(4);
   const int ntop = (int)lv.n[L - 1];
-  const Seg& yts = yseg(nl - 1);
-  const double* yt = seg_ptr<double>(sm, yts);
-  const double* Nt = seg_ptr<double>(sm, C.nn[nl - 1]);
-  const int64_t Nto = C.nn[nl - 1].org;
+  const double* yt = yl(nl - 1);
+  const double* Nt = nlv(nl - 1);
   double ysum = 0.0;
-  for (int i = threadIdx.x; i < ntop; i += CT) ysum += yt[i - yts.org];
+  for (int i = tid; i < ntop; i += CT) ysum += yt[i];
   ysum = block_sum<CT>(ysum);
   gd = block_sum<CT>(gd);
-  if (threadIdx.x == 0) sh_rho = lv.c_sum * ysum / lv.n_tilde;
+  if (tid == 0) sh_rho = lv.c_sum * ysum / lv.n_tilde;
   __syncthreads();
   const double rho = sh_rho;
-  double* tt = seg_ptr<double>(sm, C.tt);
-  for (int i = threadIdx.x; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i - yts.org] - rho * Nt[i - Nto];
+  double* tt = reinterpret_cast<double*>(sm + cd.o_tt);
+  for (int i = tid; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
   __syncthreads();
-  const double* pinv = stage_pinv ? seg_ptr<double>(sm, C.pinv) - C.pinv.org : pinv_g;
-  double* zt = seg_ptr<double>(sm, C.z[nl - 1]);
-  double* wt = seg_ptr<double>(sm, C.w[nl - 1]);
+  const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
+  double* zt = reinterpret_cast<double*>(sm + cd.o_z[nl - 1]);
+  double* wt = reinterpret_cast<double*>(sm + cd.o_w[nl - 1]);
   double nz = 0.0;
-  for (int i = threadIdx.x; i < ntop; i += CT) {
+  for (int i = tid; i < ntop; i += CT) {
     double zi = 0.0;
-    for (int j = 0; j < ntop; ++j) zi += pinv[(int64_t)i * ntop + j] * tt[j];
+    for (int j = 0; j < ntop; ++j) zi += pinv[i * ntop + j] * tt[j];
     zt[i] = zi;
-    nz += Nt[i - Nto] * zi;
+    nz += Nt[i] * zi;
   }
   nz = block_sum<CT>(nz);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     sh_m = (nz + gd - rho * lv.GN) / lv.n_tilde;
     scal[S_SHIFT] = rho;
   }
   __syncthreads();
   double rz = 0.0;
-  for (int i = threadIdx.x; i < ntop; i += CT) {
+  for (int i = tid; i < ntop; i += CT) {
     const double z = zt[i] - sh_m;
     zt[i] = z;
     wt[i] = z;
-    if (L == 1) { rz += yt[i - yts.org] * z; zout[i] = z; }
+    if (L == 1) { rz += yt[i] * z; zout[i] = z; }
   }
+  TRACE(5);
   // ---- down
+  const double negmu = lv.negmu;
   for (int t = nl - 2; t >= 0; --t) {  // child level k = Kc+t, parent k+1
     __syncthreads();
     const int k = Kc + t;
-    const int32_t* cp = seg_ptr<int32_t>(sm, C.cp[t + 1]);
-    const int64_t cpo = C.cp[t + 1].org;
-    const double* ki = seg_ptr<double>(sm, C.ki[t + 1]);
-    const int64_t kio = C.ki[t + 1].org;
-    const double* lo = seg_ptr<double>(sm, C.lo[t]);
-    const int64_t loo = C.lo[t].org;
-    const double* zp = seg_ptr<double>(sm, C.z[t + 1]);
-    const double* wp = seg_ptr<double>(sm, C.w[t + 1]);
-    const Seg& ycs = yseg(t);
-    const double* yc = seg_ptr<double>(sm, ycs);
-    const double* nc = seg_ptr<double>(sm, C.nn[t]);
-    const int64_t nco = C.nn[t].org;
-    double* zc = seg_ptr<double>(sm, C.z[t]);
-    double* wc = seg_ptr<double>(sm, C.w[t]);
+    const int* cp = reinterpret_cast<const int*>(sm + cd.o_cp[t + 1]) + skc[t + 1];
+    const double* ki = reinterpret_cast<const double*>(sm + cd.o_ki[t + 1]) + skk[t + 1];
+    const double* lo = reinterpret_cast<const double*>(sm + cd.o_lo[t]) + skl[t];
+    const double* zp = reinterpret_cast<const double*>(sm + cd.o_z[t + 1]);
+    const double* wp = reinterpret_cast<const double*>(sm + cd.o_w[t + 1]);
+    const double* yc = yl(t);
+    const double* nc = nlv(t);
+    double* zc = reinterpret_cast<double*>(sm + cd.o_z[t]);
+    double* wc = reinterpret_cast<double*>(sm + cd.o_w[t]);
     const double ckk = lv.ck[k];
     const bool out1 = (k == 1);
-    for (int64_t B = threadIdx.x; B < lv.n[k]; B += CT) {
-      const int64_t lb = 3 * (-2 * B - 2) - loo;
+    const int np = (int)lv.n[k];
+    for (int i = tid; i < np; i += CT) {
+      const int lb = -3 * (2 * i + 2);
       block_solve(
-          cp[B - cpo], cp[B + 1 - cpo], [&](int j) { return ki[3 * B + j - kio]; },
-          [&](int64_t p, int j) { return lo[lb + 3 * p + j]; }, zp[B], lv.negmu * wp[B],
-          [&](int64_t p) { return out1 ? yc[p - ycs.org] - rho : ckk * yc[p - ycs.org] - rho * nc[p - nco]; },
-          [&](int64_t p, double z, double w) {
-            if (out1) { rz += yc[p - ycs.org] * w; zout[p] = w; }
+          cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+          zp[i], negmu * wp[i], [&](int p) { return out1 ? yc[p] - rho : ckk * yc[p] - rho * nc[p]; },
+          [&](int p, double z, double w) {
+            if (out1) { rz += yc[p] * w; zout[p] = w; }
             else { zc[p] = z; wc[p] = w; }
           });
     }
   }
   __syncthreads();
+  TRACE(6);
   pdl_trigger();
   if (Kc > 1) {
-    const int64_t nk = lv.n[Kc - 1], base = lv.off[Kc - 1];
-    const double* zc = seg_ptr<double>(sm, C.z[0]);
-    const double* wc = seg_ptr<double>(sm, C.w[0]);
-    for (int64_t i = threadIdx.x; i < nk; i += CT) { Zg[base + i] = zc[i]; Wg[base + i] = wc[i]; }
+    const int nk = (int)lv.n[Kc - 1];
+    const int64_t base = lv.off[Kc - 1];
+    const double* zc = reinterpret_cast<const double*>(sm + cd.o_z[0]);
+    const double* wc = reinterpret_cast<const double*>(sm + cd.o_w[0]);
+    for (int i = tid; i < nk; i += CT) { Zg[base + i] = zc[i]; Wg[base + i] = wc[i]; }
   } else {
     rz = block_sum<CT>(rz);
-    if (threadIdx.x == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
+    if (tid == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
   }
 }
 
@@ -853,15 +944,14 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
              (const unsigned*)cnt, mode);
       P.end(PC_MID_UP);
     } else {
-      const int nl = T.k1 - T.k0 + 1;
       if (T.k0 == 1)
-        launch(k_tile_up<true>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.k0, nl, (int)T.ntiles,
-               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, q, r, (const double*)h.Hvec.p, h.Y.p, part_rr,
-               part_gd, scal, cnt, mode);
+        launch(k_tile_up<true>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.desc,
+               (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
+               part_rr, part_gd, scal, cnt, mode);
       else
-        launch(k_tile_up<false>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.k0, nl, (int)T.ntiles,
-               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, q, r, (const double*)h.Hvec.p, h.Y.p, part_rr,
-               part_gd, scal, cnt, mode);
+        launch(k_tile_up<false>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.desc,
+               (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
+               part_rr, part_gd, scal, cnt, mode);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
     }
     ++h.launches;
@@ -870,9 +960,9 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
   {
     P.begin();
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
-    launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.coarse_stage_pinv ? 1 : 0, (const int32_t*)h.cptr.p,
+    launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
            (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
-           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int64_t)h.tiers[0].ntiles, scal, cnt, mode);
+           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int)h.tiers[0].ntiles, scal, cnt, mode);
     P.end(PC_COARSE);
     ++h.launches;
   }
@@ -896,14 +986,13 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
                h.W.p + ok, part_rz, scal, cnt, mode);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
-      const int nl = T.k1 - T.k0 + 1;
       if (T.k0 == 1)
-        launch(k_tile_down<true>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.k0, nl, (int)T.ntiles,
+        launch(k_tile_down<true>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
                cnt, mode);
       else
-        launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.k0, nl, (int)T.ntiles,
+        launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode);
@@ -1108,3 +1197,9 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
 }
 
 }  // namespace msp
+
+#ifdef MSP_TRACE
+extern "C" int msp_debug_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, msp::g_trace, sizeof(msp::g_trace)) == cudaSuccess ? 0 : -2;
+}
+#endif

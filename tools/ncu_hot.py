@@ -5,9 +5,10 @@ import sys
 
 rows = list(csv.reader(sys.stdin))
 hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[0] != "Address"]
 ia, isrc, ist = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
-tot = sum(int(r[ist] or 0) for r in data)
+tot = sum(int(r[ist] or 0) for r in data if r[ist].isdigit())
+data = [r for r in data if r[ist].isdigit()]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 print("total samples", tot)
 order = sorted(range(len(data)), key=lambda i: -int(data[i][ist] or 0))[:n]

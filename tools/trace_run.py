@@ -1,0 +1,46 @@
+"""Build a -DMSP_TRACE copy of the library and run apply_R once on config 1
+(phase timestamps of CTA 0 printed by the kernels)."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2207_07847_b200 import build as B  # noqa: E402
+
+lib = os.path.join(ROOT, "build_trace_libmsp.so")
+B.build(force=True, extra=["-DMSP_TRACE"], lib=lib)
+code = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2207_07847_b200 as M
+from inputs import graphs as G
+dev = torch.device('cuda:0')
+g = G.config_graph(%d)
+S = M.setup(g.n, torch.as_tensor(g.rowptr, device=dev), torch.as_tensor(g.col, device=dev),
+            torch.as_tensor(g.val, device=dev), mu=0.8)
+r = torch.as_tensor(G.rhs(g.n, 0), device=dev)
+import ctypes, numpy as np
+L = ctypes.CDLL(%r)
+buf = np.zeros((8, 16), dtype=np.uint64)
+for _ in range(3):
+    z = S.apply_R(r); torch.cuda.synchronize()
+L.msp_debug_trace(buf.ctypes.data)
+names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>'}
+for kid, nm in names.items():
+    row = buf[kid].astype(np.int64)
+    nz = [i for i in range(16) if row[i]]
+    if nz:
+        t0 = row[nz[0]]
+        print('TRACE', nm, ' '.join(f'{i}:{(row[i]-t0)/1000:.2f}us' for i in nz))
+print('INFO', S.info())
+""" % (ROOT, int(sys.argv[1]) if len(sys.argv) > 1 else 1, lib)
+env = dict(os.environ, MSP_LIB_OVERRIDE=lib)
+out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+lines = [l for l in out.stdout.splitlines() if l.startswith("TRACE") or l.startswith("INFO")]
+print(out.stderr[-2000:])
+# last apply only: group by kernel, print deltas
+last = lines[-(len(lines) // 3 + 1):]
+prev = {}
+for l in lines:
+    print(l)
