@@ -47,7 +47,7 @@ extern "C" {
 
 #define MSP_PRECOND_NONE 0        /* plain CG (R = I)                           */
 #define MSP_PRECOND_MSP 1         /* R = P(mu) L_T~^+ P(mu)^T   (§3.3)          */
-#define MSP_PRECOND_PEGP 2        /* R = P(mu) L_H~^+ P(mu)^T   (§3.2)          */
+#define MSP_PRECOND_PEGP 2        /* R = P(mu) L_H~^+ P(mu)^T   (§3.2), inner CG */
 
 typedef struct msp_handle msp_handle;
 
@@ -140,11 +140,31 @@ int msp_apply_L(msp_handle* h, const double* x, double* y, int mem, void* stream
 /*
  * msp_apply_R -- z = R r with R = P(mu) L_X^+ P(mu)^T (reading R9):
  *   precond = MSP_PRECOND_MSP  : X = T~, exact (block-tree elimination sweeps)
+ *   precond = MSP_PRECOND_PEGP : X = H~ (§3.2, the positive subgraph of G~),
+ *                                L_H~^+ by MSP-preconditioned CG in the
+ *                                expanded space to the relative residual of
+ *                                msp_pegp_params (reading R13)
  *   precond = MSP_PRECOND_NONE : z = r
- *   precond = MSP_PRECOND_PEGP : MSP_ERR_UNSUPPORTED in this build
  * r, z: n entries in `mem`; may alias.
  */
 int msp_apply_R(msp_handle* h, int precond, const double* r, double* z, int mem, void* stream);
+
+/*
+ * Expanded-space calls (PEGP support and parity checks).  Vectors have n~
+ * entries in the canonical expanded numbering (level-k node a at
+ * sum_{j<k} n_j + a, as msp_get_msp_edges), in `mem`.
+ *   msp_apply_LH : y~ = L_H~ x~, the Laplacian of the PEGP H~ (§3.2,
+ *                  positive edges of Eq. def:L_ell), applied matrix-free.
+ *   msp_solve_LH : z~ = L_H~^+ r~ (minimum norm) by CG preconditioned with the
+ *                  exact L_T~^+ (§3.3); *inner_iterations receives the count
+ *                  (may be NULL).  Inexact: relative residual <= inner_rtol.
+ *   msp_pegp_params : inner_rtol in (0, 1) (default 1e-13) and inner_maxit
+ *                  (default 5000) of that CG.
+ * x and y (r and z) may not alias.  Errors: MSP_ERR_ARG, MSP_ERR_CUDA.
+ */
+int msp_apply_LH(msp_handle* h, const double* x, double* y, int mem, void* stream);
+int msp_solve_LH(msp_handle* h, const double* r, double* z, int mem, void* stream, int32_t* inner_iterations);
+int msp_pegp_params(msp_handle* h, double inner_rtol, int32_t inner_maxit);
 
 /*
  * msp_pcg_solve -- preconditioned CG for L_G x = b, x0 = 0, stopping at the

@@ -69,10 +69,13 @@ def _load():
     L.msp_pcg_solve.argtypes = [P, ctypes.c_int, P, P, d, i32, ctypes.c_int, P, ctypes.POINTER(_Report)]
     L.msp_set_profiling.argtypes = [P, ctypes.c_int]
     L.msp_get_profile.argtypes = [P, P, P]
+    L.msp_apply_LH.argtypes = [P, P, P, ctypes.c_int, P]
+    L.msp_solve_LH.argtypes = [P, P, P, ctypes.c_int, P, ctypes.POINTER(i32)]
+    L.msp_pegp_params.argtypes = [P, d, i32]
     L.msp_last_error.restype = ctypes.c_char_p
     for f in ("msp_setup", "msp_destroy", "msp_info", "msp_level_sizes", "msp_get_aggregates",
               "msp_get_msp_edges", "msp_apply_L", "msp_apply_R", "msp_pcg_solve", "msp_set_profiling",
-              "msp_get_profile"):
+              "msp_get_profile", "msp_apply_LH", "msp_solve_LH", "msp_pegp_params"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -217,6 +220,33 @@ class Solver:
             raise ValueError("r and z must live in the same memory space")
         _check(_lib.msp_apply_R(self._h, _PRECOND[precond], pr, pz, mr, _stream_ptr(stream)))
         return z
+
+    def n_tilde(self) -> int:
+        return int(self.info()["n_tilde"])
+
+    def pegp_params(self, inner_rtol: float = 1e-13, inner_maxit: int = 5000):
+        _check(_lib.msp_pegp_params(self._h, float(inner_rtol), int(inner_maxit)))
+
+    def apply_LH(self, x, y=None, stream=None):
+        """y~ = L_H~ x~ on expanded vectors (canonical expanded numbering)."""
+        y = _like(x) if y is None else y
+        px, mx, kx = _ptr_mem(x, np.float64)
+        py, my, ky = _ptr_mem(y, np.float64)
+        if mx != my:
+            raise ValueError("x and y must live in the same memory space")
+        _check(_lib.msp_apply_LH(self._h, px, py, mx, _stream_ptr(stream)))
+        return y
+
+    def solve_LH(self, r, z=None, stream=None):
+        """z~ = L_H~^+ r~ (inner CG); returns (z~, inner iterations)."""
+        z = _like(r) if z is None else z
+        pr, mr, kr = _ptr_mem(r, np.float64)
+        pz, mz, kz = _ptr_mem(z, np.float64)
+        if mr != mz:
+            raise ValueError("r and z must live in the same memory space")
+        it = ctypes.c_int32(0)
+        _check(_lib.msp_solve_LH(self._h, pr, pz, mr, _stream_ptr(stream), ctypes.byref(it)))
+        return z, it.value
 
     def pcg_solve(self, b, x=None, rtol: float = 1e-8, maxit: int = 100000, precond="msp",
                   stream=None) -> dict:

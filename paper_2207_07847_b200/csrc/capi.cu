@@ -227,14 +227,13 @@ int msp_apply_R(msp_handle* H, int precond, const double* r, double* z, int mem,
   return guarded([&] {
     need(H && r && z, "null argument");
     need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
-    if (precond == MSP_PRECOND_PEGP)
-      throw Error{MSP_ERR_UNSUPPORTED, "PEGP apply is not in this build"};
-    need(precond == MSP_PRECOND_MSP || precond == MSP_PRECOND_NONE, "bad precond");
+    need(precond == MSP_PRECOND_MSP || precond == MSP_PRECOND_NONE || precond == MSP_PRECOND_PEGP, "bad precond");
     Handle& h = H->h;
     cudaStream_t st = S(stream);
     const double* rd = stage_in(h, r, mem, h.stage_in, st);
     msp::gather_to_nested(h, rd, h.vr.p, st);
     if (precond == MSP_PRECOND_MSP) msp::apply_R_msp_nested(h, h.vr.p, h.vz.p, st);
+    else if (precond == MSP_PRECOND_PEGP) msp::apply_R_pegp_nested(h, h.vr.p, h.vz.p, st);
     else MSP_CUDA(cudaMemcpyAsync(h.vz.p, h.vr.p, h.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (mem == MSP_MEM_DEVICE) {
       msp::scatter_from_nested(h, h.vz.p, z, st);
@@ -253,9 +252,7 @@ int msp_pcg_solve(msp_handle* H, int precond, const double* b, double* x, double
     need(H && b && x, "null argument");
     need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
     need(rtol >= 0 && maxit >= 0, "bad rtol / maxit");
-    if (precond == MSP_PRECOND_PEGP)
-      throw Error{MSP_ERR_UNSUPPORTED, "PEGP apply is not in this build"};
-    need(precond == MSP_PRECOND_MSP || precond == MSP_PRECOND_NONE, "bad precond");
+    need(precond == MSP_PRECOND_MSP || precond == MSP_PRECOND_NONE || precond == MSP_PRECOND_PEGP, "bad precond");
     Handle& h = H->h;
     cudaStream_t st = S(stream);
     const double* bd = stage_in(h, b, mem, h.stage_in, st);
@@ -270,6 +267,72 @@ int msp_pcg_solve(msp_handle* H, int precond, const double* b, double* x, double
       MSP_CUDA(cudaMemcpyAsync(x, h.stage_out.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, st));
       MSP_CUDA(cudaStreamSynchronize(st));
     }
+  });
+}
+
+int msp_pegp_params(msp_handle* H, double inner_rtol, int32_t inner_maxit) {
+  return guarded([&] {
+    need(H != nullptr, "null handle");
+    need(inner_rtol > 0 && inner_rtol < 1 && inner_maxit > 0, "bad PEGP parameters");
+    H->h.pegp_rtol = inner_rtol;
+    H->h.pegp_maxit = inner_maxit;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// run f(x_nested, y_nested) on expanded vectors given in the canonical
+// expanded numbering (n~ entries in `mem`)
+template <typename F>
+void expanded_call(Handle& h, const double* x, double* y, int mem, cudaStream_t st, F&& f) {
+  const int64_t nt = h.n_tilde;
+  msp::pegp_build(h, st);
+  DBuf<double> xin, xn, yn, yout;
+  xn.alloc(nt + 8);
+  yn.alloc(nt + 8);
+  const double* xd = x;
+  if (mem == MSP_MEM_HOST) {
+    xin.alloc(nt);
+    MSP_CUDA(cudaMemcpyAsync(xin.p, x, nt * sizeof(double), cudaMemcpyHostToDevice, st));
+    xd = xin.p;
+  }
+  msp::expanded_to_nested(h, xd, xn.p, st);
+  f(xn.p, yn.p);
+  if (mem == MSP_MEM_DEVICE) {
+    msp::nested_to_expanded(h, yn.p, y, st);
+  } else {
+    yout.alloc(nt);
+    msp::nested_to_expanded(h, yn.p, yout.p, st);
+    MSP_CUDA(cudaMemcpyAsync(y, yout.p, nt * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  MSP_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+extern "C" {
+
+int msp_apply_LH(msp_handle* H, const double* x, double* y, int mem, void* stream) {
+  return guarded([&] {
+    need(H && x && y, "null argument");
+    need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
+    Handle& h = H->h;
+    expanded_call(h, x, y, mem, S(stream), [&](const double* xn, double* yn) {
+      msp::apply_LH_nested(h, xn, yn, S(stream));
+    });
+  });
+}
+
+int msp_solve_LH(msp_handle* H, const double* r, double* z, int mem, void* stream, int32_t* inner_iterations) {
+  return guarded([&] {
+    need(H && r && z, "null argument");
+    need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
+    Handle& h = H->h;
+    int it = 0;
+    expanded_call(h, r, z, mem, S(stream), [&](const double* rn, double* zn) {
+      it = msp::solve_LH_nested(h, rn, zn, S(stream));
+    });
+    if (inner_iterations) *inner_iterations = it;
   });
 }
 

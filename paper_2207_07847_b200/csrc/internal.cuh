@@ -138,6 +138,19 @@ struct Handle {
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
 
+  // ---- PEGP (built lazily on first use, pegp.cu)
+  bool pegp_ready = false;
+  DBuf<int32_t> parent;       // [n~]: expanded index of the parent aggregate, -1 on top
+  DBuf<int64_t> hrow;         // per-level adjacency over n~ (nested, absolute columns)
+  DBuf<int32_t> hcol;
+  DBuf<double> hw;
+  int64_t hnnz = 0;
+  DBuf<double> ex, er, ep, eq, ez, es, ey;  // expanded-space CG vectors
+  DBuf<double> edots, epart;
+  double pegp_rtol = 1e-13;
+  int pegp_maxit = 5000;
+  int pegp_last_inner = 0;
+
   // ---- solve workspaces
   DBuf<double> Y, Z, W;       // n~-layout sweep vectors (y = P^T sums, z, w)
   DBuf<double> red;           // reduction partials
@@ -181,6 +194,14 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
                 cudaStream_t st, msp_report* rep);
 void alloc_solve_workspace(Handle& h);
 void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
+// pegp.cu
+void pegp_build(Handle& h, cudaStream_t st);
+void apply_LH_nested(Handle& h, const double* x, double* y, cudaStream_t st);
+void apply_LT_pinv_nested(Handle& h, const double* rt, double* z, cudaStream_t st);
+int solve_LH_nested(Handle& h, const double* rt, double* z, cudaStream_t st);
+void apply_R_pegp_nested(Handle& h, const double* r, double* z, cudaStream_t st);
+void expanded_to_nested(Handle& h, const double* src, double* dst, cudaStream_t st);
+void nested_to_expanded(Handle& h, const double* src, double* dst, cudaStream_t st);
 Lv make_level_table(const Handle& h);              // setup.cu
 void release_graph(Handle& h);
 

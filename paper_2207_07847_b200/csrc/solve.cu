@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
 // R = I: r -= alpha q, rr; z = r so rz = rr -> beta  (x deferred into L p)
 __global__ void __launch_bounds__(TPB) k_update_cg(int64_t n, double* __restrict__ r, const double* __restrict__ q,
                                                    double* __restrict__ part, double* __restrict__ scal,
-                                                   unsigned int* __restrict__ cnt, int mode) {
+                                                   unsigned int* __restrict__ cnt, int mode, int set_rz) {
   pdl_wait();
   if (mode == M_ITER && cnt[C_DONE]) return;
   const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
@@ -849,9 +849,25 @@ __global__ void __launch_bounds__(TPB) k_update_cg(int64_t n, double* __restrict
     const double rr = block_sum_partials<TPB>(part, gridDim.x);
     if (threadIdx.x == 0) {
       finish_rr(rr, scal, cnt, mode);
-      if (!cnt[C_DONE]) finish_rz(rr, scal, mode);
+      if (set_rz && !cnt[C_DONE]) finish_rz(rr, scal, mode);
       cnt[C_UPD] = 0;
     }
+  }
+}
+
+// rz = (r, z) after an externally applied preconditioner -> beta, rho
+__global__ void __launch_bounds__(TPB) k_rz(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
+                                            double* __restrict__ part, double* __restrict__ scal,
+                                            unsigned int* __restrict__ cnt, int mode) {
+  pdl_wait();
+  double d = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d += r[i] * z[i];
+  d = block_sum<TPB>(d);
+  if (threadIdx.x == 0) part[blockIdx.x] = d;
+  if (last_block(&cnt[C_DOWN])) {
+    const double rz = block_sum_partials<TPB>(part, gridDim.x);
+    if (threadIdx.x == 0) { finish_rz(rz, scal, mode); cnt[C_DOWN] = 0; }
   }
 }
 
@@ -1027,7 +1043,7 @@ void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t
   } else {
     P.begin();
     launch(k_update_cg, std::min<unsigned>(grid_for(h.n), 148u * 8u), TPB, 0, st, h.n, h.vr.p,
-           (const double*)h.vq.p, h.red.p, h.scal.p, h.counters.p, (int)M_ITER);
+           (const double*)h.vq.p, h.red.p, h.scal.p, h.counters.p, (int)M_ITER, 1);
     P.end(PC_TILE_UP);
     ++h.launches;
   }
@@ -1123,18 +1139,49 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
     Prof P(h, st);
     if (precond == MSP_PRECOND_MSP) {
       msp_sweeps(h, lv, nullptr, h.vr.p, h.vz.p, st, M_INIT, P);
-    } else {
+    } else if (precond == MSP_PRECOND_NONE) {
       launch(k_update_cg, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, h.vr.p, (const double*)nullptr,
-             h.red.p, h.scal.p, h.counters.p, (int)M_INIT);
+             h.red.p, h.scal.p, h.counters.p, (int)M_INIT, 1);
       ++h.launches;
     }
   }
+  unsigned host_cnt[C_NCNT];
+  if (precond == MSP_PRECOND_PEGP) {
+    // PEGP: the inner solve is host-driven, so iterations run one by one
+    unsigned hc[C_NCNT];
+    auto flag = [&]() {
+      MSP_CUDA(cudaMemcpyAsync(hc, h.counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+      return hc[C_DONE] != 0;
+    };
+    const unsigned gv = std::min<unsigned>(grid_for(n), 148u * 8u);
+    launch(k_update_cg, gv, TPB, 0, st, n, h.vr.p, (const double*)nullptr, h.red.p, h.scal.p, h.counters.p,
+           (int)M_INIT, 0);
+    if (!flag()) {
+      apply_R_pegp_nested(h, h.vr.p, h.vz.p, st);
+      launch(k_rz, gv, TPB, 0, st, n, (const double*)h.vr.p, (const double*)h.vz.p, h.red.p, h.scal.p, h.counters.p,
+             (int)M_INIT);
+      for (int it = 0; it < maxit; ++it) {
+        double* pold = h.pparity ? h.vp2.p : h.vp.p;
+        double* pnew = h.pparity ? h.vp.p : h.vp2.p;
+        h.pparity ^= 1;
+        launch_spmv<true>(h, h.vz.p, pold, pnew, h.vq.p, x, st);
+        launch(k_update_cg, gv, TPB, 0, st, n, h.vr.p, (const double*)h.vq.p, h.red.p, h.scal.p, h.counters.p,
+               (int)M_ITER, 0);
+        h.launches += 2;
+        if (flag()) break;
+        apply_R_pegp_nested(h, h.vr.p, h.vz.p, st);
+        launch(k_rz, gv, TPB, 0, st, n, (const double*)h.vr.p, (const double*)h.vz.p, h.red.p, h.scal.p,
+               h.counters.p, (int)M_ITER);
+        ++h.launches;
+      }
+    }
+  } else {
   // iterations in batches; a batch is a captured CUDA graph (even length so
   // the p / p_old ping-pong is periodic), the done flag read once per batch
   int batch = 32;
   if (const char* e = std::getenv("MSP_PCG_BATCH")) batch = std::max(2, std::atoi(e) & ~1);
   const bool use_graph = !h.profile && std::getenv("MSP_NO_GRAPH") == nullptr;
-  unsigned host_cnt[C_NCNT];
   int it = 0;
   Prof P(h, st);
   while (it < maxit) {
@@ -1174,6 +1221,7 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
     MSP_CUDA(cudaMemcpyAsync(host_cnt, h.counters.p, sizeof(host_cnt), cudaMemcpyDeviceToHost, st));
     MSP_CUDA(cudaStreamSynchronize(st));
     if (host_cnt[C_DONE]) break;
+  }
   }
   launch(k_x_final, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, x, (const double*)h.vp.p,
          (const double*)h.vp2.p, (const double*)h.scal.p, (const unsigned*)h.counters.p);

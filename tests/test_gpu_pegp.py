@@ -1,0 +1,119 @@
+"""GPU parity of the PEGP path (§3.2) against the oracle.
+
+* msp_apply_LH: the matrix-free L_H~ x~ equals the oracle's assembled L_H~
+  (positive edges of Eq. def:L_ell) within 1e-12 relative (fp64).
+* msp_solve_LH: inexact by construction (reading R13): the inner CG's
+  residual in the L_H~ system is <= inner_rtol (checked with the oracle's
+  L_H~), and the result agrees with the oracle's pseudo-inverse solve within
+  the bound that residual implies.
+* apply_R PEGP and PCG with PEGP against the oracle's exact PEGP.
+"""
+import numpy as np
+import pytest
+
+from inputs import graphs as G
+from oracle import aggregation as A
+from oracle import expansion as E
+from oracle import graph as GR
+from oracle import pcg as PC
+from oracle import precond as PR
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2207_07847_b200 as M  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def dt(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=DEV)
+
+
+GRAPHS = {
+    "grid_9x7_loguniform": lambda: G.grid2d(9, 7, "loguniform", 1),
+    "grid_20x13_u1_10": lambda: G.grid2d(20, 13, "uniform1_10", 2),
+    "ws_300": lambda: G.watts_strogatz(300, 4, None, 1),
+    "rgg_800": lambda: G.rgg(800, 12.0, 3),
+    "chung_lu_600": lambda: G.chung_lu(600, 2.1, 16.0, 4),
+    "grid3d_6": lambda: G.grid3d(6, 5, 4, seed=1),
+}
+
+
+@pytest.fixture(scope="module", params=list(GRAPHS))
+def case(request):
+    g = GRAPHS[request.param]()
+    mu, seed = 0.8, 5
+    h = A.build_hierarchy(g, seed)
+    sysm = E.expand(g, h, mu)
+    s = M.setup(g.n, dt(g.rowptr, torch.int64), dt(g.col, torch.int32), dt(g.val), mu=mu, seed=seed)
+    return request.param, g, h, sysm, s
+
+
+def test_apply_LH(case):
+    name, g, h, sysm, s = case
+    LH = sysm.LH
+    for seed in (0, 1):
+        x = np.random.default_rng(seed).standard_normal(h.n_tilde)
+        y = s.apply_LH(dt(x)).cpu().numpy()
+        ref = LH @ x
+        assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max(), name
+
+
+@pytest.mark.parametrize("mu", [0.3, 0.5])
+def test_apply_LH_other_mu(mu):
+    g = G.grid2d(11, 10, "loguniform", 6)
+    h = A.build_hierarchy(g, 2)
+    sysm = E.expand(g, h, mu)
+    s = M.setup(g.n, dt(g.rowptr, torch.int64), dt(g.col, torch.int32), dt(g.val), mu=mu, seed=2)
+    x = np.random.default_rng(3).standard_normal(h.n_tilde)
+    ref = sysm.LH @ x
+    assert np.abs(s.apply_LH(dt(x)).cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_solve_LH(case):
+    name, g, h, sysm, s = case
+    LH = sysm.LH
+    r = np.random.default_rng(7).standard_normal(h.n_tilde)
+    r -= r.mean()
+    s.pegp_params(1e-13, 5000)
+    z, it = s.solve_LH(dt(r))
+    z = z.cpu().numpy()
+    assert it > 0
+    res = np.linalg.norm(LH @ z - r)
+    assert res <= 2e-13 * np.linalg.norm(r), (name, res / np.linalg.norm(r), it)
+    assert abs(z.sum()) <= 1e-10 * np.abs(z).sum()
+    zref = PR.PinvSolver(LH)(r)
+    # ||z - z*|| <= ||L_H (z - z*)|| / lambda_2(L_H)
+    lam2 = np.sort(np.linalg.eigvalsh(LH.toarray()))[1]
+    assert np.linalg.norm(z - zref) <= 1.5 * res / lam2 + 1e-12 * np.linalg.norm(zref), name
+
+
+def test_apply_R_pegp(case):
+    name, g, h, sysm, s = case
+    s.pegp_params(1e-14, 5000)
+    R = PR.pegp(sysm)
+    r = G.rhs(g.n, 8)
+    z = s.apply_R(dt(r), precond="pegp").cpu().numpy()
+    zr = R(r)
+    # inner solve inexact (R13): bound from the L_H~ residual it reaches
+    assert np.abs(z - zr).max() <= 1e-9 * np.abs(zr).max(), (name, np.abs(z - zr).max() / np.abs(zr).max())
+
+
+def test_pcg_pegp(case):
+    name, g, h, sysm, s = case
+    s.pegp_params(1e-14, 5000)
+    L = GR.laplacian_of_graph(g)
+    b = G.rhs(g.n, 9)
+    ref = PC.pcg(lambda v: L @ v, b, PR.pegp(sysm), 1e-8, 2000)
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=2000, precond="pegp")
+    assert out["converged"] == 1 and ref.converged
+    assert abs(out["iterations"] - ref.iterations) <= 2, (name, out["iterations"], ref.iterations)
+    x = out["x"].cpu().numpy()
+    e = x - ref.x
+    e -= e.mean()
+    xs = ref.x - ref.x.mean()
+    assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs)), name
