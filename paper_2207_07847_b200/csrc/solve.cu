@@ -41,7 +41,10 @@ constexpr int TPB = 256;      // SpMV and per-node kernels
 #define MSP_TT 128
 #endif
 constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
-constexpr int CT = 1024;      // coarse kernel (single CTA)
+#ifndef MSP_CT
+#define MSP_CT 1024
+#endif
+constexpr int CT = MSP_CT;    // coarse kernel (single CTA)
 
 // device scalar slots
 enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S_NSCAL };
@@ -138,6 +141,27 @@ __device__ __forceinline__ double block_sum(double v) {
   return tot;
 }
 
+// block-wide sum of two values at once
+template <int NT>
+__device__ __forceinline__ double2 block_sum2(double2 v) {
+  __shared__ double2 ws2[NT / 32];
+  __shared__ double2 tot2;
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) ws2[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double2 t = (lane < NT / 32) ? ws2[lane] : make_double2(0.0, 0.0);
+    t.x = warp_sum(t.x);
+    t.y = warp_sum(t.y);
+    if (lane == 0) tot2 = t;
+  }
+  __syncthreads();
+  return tot2;
+}
+
 // deterministic sum of partials[0..n) written by other blocks (L2 reads)
 template <int NT>
 __device__ __forceinline__ double block_sum_partials(const double* part, int64_t n) {
@@ -158,6 +182,25 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
   }
   __syncthreads();
   return is_last;
+}
+
+// Warp-level ticket: lane 0 publishes this block's partial (already stored)
+// and takes a ticket; true in every lane of the warp that arrives last.
+__device__ __forceinline__ bool warp_last_block(unsigned int* counter) {
+  unsigned last = 0;
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (last) __threadfence();
+  }
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+// fixed-order sum of partials[0..n) by one warp (all lanes get the result)
+__device__ __forceinline__ double warp_sum_partials(const double* part, int64_t n) {
+  double v = 0.0;
+  for (int64_t i = threadIdx.x & 31; i < n; i += 32) v += __ldcg(part + i);
+  return warp_sum(v);
 }
 
 // Exact solve of one aggregate of T~: children [s0, s1) (matched pair s0,
@@ -227,8 +270,11 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ perm, const dou
 // y_i = sum_j w_ij (x_i - x_j)   (L_G = B^T W B, §2.1), SELL-32.
 // PCG: p = z + beta p_old (rows and gathered neighbours alike), q = L_G p,
 // (p, q) -> alpha = rho / (p, q); and the deferred x += alpha_prev p_old.
+#ifndef MSP_SPMV_MINB
+#define MSP_SPMV_MINB 8
+#endif
 template <bool PCG>
-__global__ void __launch_bounds__(TPB) k_spmv(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
+__global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                               const int32_t* __restrict__ scol, const double* __restrict__ sw,
                                               const uint32_t* __restrict__ smask, int64_t nlong,
                                               const int32_t* __restrict__ long_rows,
@@ -297,13 +343,15 @@ __global__ void __launch_bounds__(TPB) k_spmv(int64_t n, int64_t nslices, const 
   if (!PCG) return;
   pdl_trigger();
   const double bs = block_sum<TPB>(d);
-  if (threadIdx.x == 0) part[blockIdx.x] = bs;
-  if (last_block(&cnt[C_SPMV])) {
-    const double pq = block_sum_partials<TPB>(part, gridDim.x);
-    if (threadIdx.x == 0) {
-      scal[S_PQ] = pq;
-      scal[S_ALPHA] = scal[S_RHO] / pq;
-      cnt[C_SPMV] = 0;
+  if (threadIdx.x < 32) {  // only warp 0 waits on the ticket
+    if (threadIdx.x == 0) part[blockIdx.x] = bs;
+    if (warp_last_block(&cnt[C_SPMV])) {
+      const double pq = warp_sum_partials(part, gridDim.x);
+      if (threadIdx.x == 0) {
+        scal[S_PQ] = pq;
+        scal[S_ALPHA] = scal[S_RHO] / pq;
+        cnt[C_SPMV] = 0;
+      }
     }
   }
 }
@@ -321,6 +369,19 @@ __global__ void k_x_final(int64_t n, double* __restrict__ x, const double* __res
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] += alpha * p[i];
 }
+
+// per-level shared-memory pointers of a tile / of the coarse levels
+// (byte offsets from the dynamic shared-memory base, so the compiler keeps
+// shared-space loads; -1 = absent)
+struct LvlPtr {
+  int cp;            // child pointers of this level's nodes (as parents)
+  int ki;            // K'^{-1} triples of this level's aggregates
+  int lo;            // leftover triples of this level's nodes (as children)
+  int y, nn, z, w;
+  int a, cnt;        // first node, node count
+  double ck;         // c(k)
+};
+#define SMP(T, off) reinterpret_cast<T*>(sm + (off))
 
 // ------------------------------------------------------------ tile staging
 // Stage [lo, hi) of a global array (absolute element indices, element size
@@ -385,16 +446,32 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   if (FIRST && !done) {  // level-1 update, overlapping the TMA of the descendant offsets
     const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
     const int a1 = sa0, n1 = sn0;
-    for (int i = tid; i < n1; i += TT) {
-      const int gi = a1 + i;
-      double ri = r[gi];
-      if (mode == M_ITER) {
-        ri -= alpha * q[gi];
-        r[gi] = ri;
+    constexpr int U = 4;  // all loads of U elements issued before any use
+    for (int i0 = tid; i0 < n1; i0 += U * TT) {
+      double rv[U], qv[U], hv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * TT;
+        if (i < n1) {
+          rv[u] = r[a1 + i];
+          qv[u] = (mode == M_ITER) ? q[a1 + i] : 0.0;
+          hv[u] = H[a1 + i];
+        }
       }
-      rr += ri * ri;
-      gd += H[gi] * ri;
-      if (nl > 1) y0[i] = ri;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * TT;
+        if (i < n1) {
+          double ri = rv[u];
+          if (mode == M_ITER) {
+            ri -= alpha * qv[u];
+            r[a1 + i] = ri;
+          }
+          rr += ri * ri;
+          gd += hv[u] * ri;
+          if (nl > 1) y0[i] = ri;
+        }
+      }
     }
   }
   mbar_wait(&bar, 0);
@@ -415,14 +492,15 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   }
   pdl_trigger();
   if (FIRST) {
-    rr = block_sum<TT>(rr);
-    gd = block_sum<TT>(gd);
-    if (tid == 0) { part_rr[tile] = rr; part_gd[tile] = gd; }
-    if (mode != M_APPLY && last_block(&cnt[C_UPD])) {
-      const double tot = block_sum_partials<TT>(part_rr, gridDim.x);
-      if (tid == 0) {
-        finish_rr(tot, scal, cnt, mode);
-        cnt[C_UPD] = 0;
+    const double2 v = block_sum2<TT>(make_double2(rr, gd));
+    if (tid < 32) {  // only warp 0 waits on the ticket
+      if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
+      if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
+        const double tot = warp_sum_partials(part_rr, gridDim.x);
+        if (tid == 0) {
+          finish_rr(tot, scal, cnt, mode);
+          cnt[C_UPD] = 0;
+        }
       }
     }
   }
@@ -446,6 +524,8 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   __shared__ __align__(8) uint64_t bar;
   __shared__ int sa[MAXT], sn[MAXT], skc[MAXT], skk[MAXT], skl[MAXT];
   __shared__ int sky0, skn0, skz, skw, sdone;
+  __shared__ double srho;
+  __shared__ LvlPtr tb[MAXT];
   const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
@@ -483,42 +563,55 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   TRACE(1);
   pdl_wait();
   TRACE(2);
-  if (tid == 0) sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
-  __syncthreads();
-  const int done = sdone;
-  if (!done) {  // dynamic segments: y_k0, z and w at level k1
-    if (g == 3 * m1 + 1) {
-      const int64_t base = FIRST ? 0 : lv.off[k0 - 1];
-      sky0 = stage_window(&bar, sm + td.o_y[0], y0src, 8, base + sa[0], base + sa[0] + sn[0]);
-    } else if (g == 3 * m1 + 2 || g == 3 * m1 + 3) {
-      const bool isz = (g == 3 * m1 + 2);
-      const int64_t base = lv.off[k0 + nl - 2] + sa[nl - 1];
-      const int v = stage_window(&bar, sm + (isz ? td.o_z[nl - 1] : td.o_w[nl - 1]), isz ? Zg : Wg, 8, base,
-                                 base + sn[nl - 1]);
-      if (isz) skz = v; else skw = v;
-    }
+  // dynamic segments (y_k0, z and w at level k1) go out at once; the done
+  // flag and rho are read alongside (a finished solve only wastes the copies)
+  if (tid == 0) {
+    sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+    srho = scal[S_SHIFT];
+  }
+  if (g == 3 * m1 + 1) {
+    const int64_t base = FIRST ? 0 : lv.off[k0 - 1];
+    sky0 = stage_window(&bar, sm + td.o_y[0], y0src, 8, base + sa[0], base + sa[0] + sn[0]);
+  } else if (g == 3 * m1 + 2 || g == 3 * m1 + 3) {
+    const bool isz = (g == 3 * m1 + 2);
+    const int64_t base = lv.off[k0 + nl - 2] + sa[nl - 1];
+    const int v = stage_window(&bar, sm + (isz ? td.o_z[nl - 1] : td.o_w[nl - 1]), isz ? Zg : Wg, 8, base,
+                               base + sn[nl - 1]);
+    if (isz) skz = v; else skw = v;
   }
   __syncthreads();
+  const int done = sdone;
   if (tid == 0) mbar_arrive(&bar);
   mbar_wait(&bar, 0);
   TRACE(3);
   if (done) return;
 
-  auto ylev = [&](int t) -> double* {
-    return reinterpret_cast<double*>(sm + td.o_y[t]) + (t == 0 ? sky0 : 0);
-  };
-  auto nlev = [&](int t) -> double* {
-    return reinterpret_cast<double*>(sm + td.o_n[t]) + (t == 0 ? skn0 : 0);
-  };
+  // per-level pointer table (one thread per level), so every phase starts
+  // with a handful of independent shared-memory loads
+  if (tid < nl) {
+    const int t = tid;
+    LvlPtr e;
+    e.cp = (t >= 1) ? td.o_cp[t] + 4 * skc[t] : -1;
+    e.ki = (t >= 1) ? td.o_ki[t] + 8 * skk[t] : -1;
+    e.lo = (t + 1 < nl) ? td.o_lo[t] + 8 * skl[t] : -1;
+    e.y = (t == 0) ? td.o_y[0] + 8 * sky0 : (t + 1 < nl ? td.o_y[t] : -1);
+    e.nn = (t == 0) ? (FIRST ? -1 : td.o_n[0] + 8 * skn0) : (t + 1 < nl ? td.o_n[t] : -1);
+    e.z = (t == nl - 1) ? td.o_z[t] + 8 * skz : (t >= 1 ? td.o_z[t] : -1);
+    e.w = (t == nl - 1) ? td.o_w[t] + 8 * skw : (t >= 1 ? td.o_w[t] : -1);
+    e.a = sa[t];
+    e.cnt = sn[t];
+    e.ck = lv.ck[k0 + t];
+    tb[t] = e;
+  }
   // ---- recompute y and N of levels k0+1 .. k1-1
   for (int t = 1; t + 1 < nl; ++t) {
     __syncthreads();
-    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[t]) + skc[t];
-    const double* yc = ylev(t - 1);
-    const double* nc = (t == 1 && FIRST) ? nullptr : nlev(t - 1);
-    double* yp = ylev(t);
-    double* np = nlev(t);
-    const int ac = sa[t - 1], npar = sn[t];
+    const int* cp = SMP(const int, tb[t].cp);
+    const double* yc = SMP(const double, tb[t - 1].y);
+    const double* nc = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
+    double* yp = SMP(double, tb[t].y);
+    double* np = SMP(double, tb[t].nn);
+    const int ac = tb[t - 1].a, npar = tb[t].cnt;
     for (int i = tid; i < npar; i += TT) {
       const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
       double y = 0.0, N = 1.0;
@@ -532,23 +625,22 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   }
   TRACE(4);
   // ---- down: levels k1-1 .. k0+1 in shared memory, then level k0 out
-  const double rho = scal[S_SHIFT];
+  const double rho = srho;
   const double negmu = lv.negmu;
   double rz = 0.0;
   for (int t = nl - 2; t >= 1; --t) {  // child level k = k0+t, parent level k+1
     __syncthreads();
-    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[t + 1]) + skc[t + 1];
-    const double* ki = reinterpret_cast<const double*>(sm + td.o_ki[t + 1]) + skk[t + 1];
-    const double* lo = reinterpret_cast<const double*>(sm + td.o_lo[t]) + skl[t];
-    const bool top = (t + 1 == nl - 1);
-    const double* zp = reinterpret_cast<const double*>(sm + td.o_z[t + 1]) + (top ? skz : 0);
-    const double* wp = reinterpret_cast<const double*>(sm + td.o_w[t + 1]) + (top ? skw : 0);
-    const double* yc = reinterpret_cast<const double*>(sm + td.o_y[t]);
-    const double* nc = reinterpret_cast<const double*>(sm + td.o_n[t]);
-    double* zc = reinterpret_cast<double*>(sm + td.o_z[t]);
-    double* wc = reinterpret_cast<double*>(sm + td.o_w[t]);
-    const int ac = sa[t], npar = sn[t + 1];
-    const double ckk = lv.ck[k0 + t];
+    const int* cp = SMP(const int, tb[t + 1].cp);
+    const double* ki = SMP(const double, tb[t + 1].ki);
+    const double* zp = SMP(const double, tb[t + 1].z);
+    const double* wp = SMP(const double, tb[t + 1].w);
+    const double* lo = SMP(const double, tb[t].lo);
+    const double* yc = SMP(const double, tb[t].y);
+    const double* nc = SMP(const double, tb[t].nn);
+    double* zc = SMP(double, tb[t].z);
+    double* wc = SMP(double, tb[t].w);
+    const int ac = tb[t].a, npar = tb[t + 1].cnt;
+    const double ckk = tb[t].ck;
     for (int i = tid; i < npar; i += TT) {
       const int lb = -3 * (2 * i + 2);
       block_solve(
@@ -560,16 +652,15 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   }
   {
     __syncthreads();
-    const int* cp = reinterpret_cast<const int*>(sm + td.o_cp[1]) + skc[1];
-    const double* ki = reinterpret_cast<const double*>(sm + td.o_ki[1]) + skk[1];
-    const double* lo = reinterpret_cast<const double*>(sm + td.o_lo[0]) + skl[0];
-    const bool top = (nl == 2);
-    const double* zp = reinterpret_cast<const double*>(sm + td.o_z[1]) + (top ? skz : 0);
-    const double* wp = reinterpret_cast<const double*>(sm + td.o_w[1]) + (top ? skw : 0);
-    const double* yc = reinterpret_cast<const double*>(sm + td.o_y[0]) + sky0;
-    const double* nc = reinterpret_cast<const double*>(sm + td.o_n[0]) + skn0;
-    const int ac = sa[0], npar = sn[1];
-    const double ckk = lv.ck[k0];
+    const int* cp = SMP(const int, tb[1].cp);
+    const double* ki = SMP(const double, tb[1].ki);
+    const double* zp = SMP(const double, tb[1].z);
+    const double* wp = SMP(const double, tb[1].w);
+    const double* lo = SMP(const double, tb[0].lo);
+    const double* yc = SMP(const double, tb[0].y);
+    const double* nc = SMP(const double, tb[0].nn >= 0 ? tb[0].nn : 0);
+    const int ac = tb[0].a, npar = tb[1].cnt;
+    const double ckk = tb[0].ck;
     double* zg = FIRST ? zout + ac : Zg + lv.off[k0 - 1] + ac;
     double* wg = Wg + lv.off[k0 - 1] + ac;
     for (int i = tid; i < npar; i += TT) {
@@ -592,10 +683,12 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   pdl_trigger();
   if (FIRST) {
     rz = block_sum<TT>(rz);
-    if (tid == 0) part[tile] = rz;
-    if (mode != M_APPLY && last_block(&cnt[C_DOWN])) {
-      const double tot = block_sum_partials<TT>(part, gridDim.x);
-      if (tid == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+    if (tid < 32) {  // only warp 0 waits on the ticket
+      if (tid == 0) part[tile] = rz;
+      if (mode != M_APPLY && warp_last_block(&cnt[C_DOWN])) {
+        const double tot = warp_sum_partials(part, gridDim.x);
+        if (tid == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+      }
     }
   }
 }
@@ -675,7 +768,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   __shared__ __align__(8) uint64_t bar;
   __shared__ int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
   __shared__ int sky0, skp, sdone;
-  __shared__ double sh_rho, sh_m;
+  __shared__ LvlPtr tb[MAXT + 8];
   const int L = lv.L, Kc = lv.Kc, nl = cd.nl, tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   TRACE(0);
@@ -726,15 +819,28 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   TRACE(3);
   if (done) return;
 
-  auto yl = [&](int t) -> double* { return reinterpret_cast<double*>(sm + cd.o_y[t]) + (t == 0 ? sky0 : 0); };
-  auto nlv = [&](int t) -> const double* { return reinterpret_cast<const double*>(sm + cd.o_n[t]) + skn[t]; };
+  if (tid < nl) {  // per-level pointer table
+    const int t = tid;
+    LvlPtr e;
+    e.cp = (t >= 1) ? cd.o_cp[t] + 4 * skc[t] : -1;
+    e.ki = (t >= 1) ? cd.o_ki[t] + 8 * skk[t] : -1;
+    e.lo = (t + 1 < nl) ? cd.o_lo[t] + 8 * skl[t] : -1;
+    e.y = cd.o_y[t] + (t == 0 ? 8 * sky0 : 0);
+    e.nn = cd.o_n[t] + 8 * skn[t];
+    e.z = cd.o_z[t];
+    e.w = cd.o_w[t];
+    e.a = 0;
+    e.cnt = (int)lv.n[Kc + t - 1];
+    e.ck = lv.ck[Kc + t];
+    tb[t] = e;
+  }
   // ---- up
   for (int t = 1; t < nl; ++t) {  // child level Kc+t-1, parent Kc+t
     __syncthreads();
-    const int* cp = reinterpret_cast<const int*>(sm + cd.o_cp[t]) + skc[t];
-    const double* yc = yl(t - 1);
-    double* yp = yl(t);
-    const int np = (int)lv.n[Kc + t - 1];
+    const int* cp = SMP(const int, tb[t].cp);
+    const double* yc = SMP(const double, tb[t - 1].y);
+    double* yp = SMP(double, tb[t].y);
+    const int np = tb[t].cnt;
     for (int i = tid; i < np; i += CT) {
       double y = 0.0;
       const int c1 = cp[i + 1];
@@ -744,23 +850,23 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   }
   // ---- top solve
   __syncthreads();
-  TRACE(4);
-  const int ntop = (int)lv.n[L - 1];
-  const double* yt = yl(nl - 1);
-  const double* Nt = nlv(nl - 1);
+  const int ntop = tb[nl - 1].cnt;
+  const double* yt = SMP(const double, tb[nl - 1].y);
+  const double* Nt = SMP(const double, tb[nl - 1].nn);
   double ysum = 0.0;
   for (int i = tid; i < ntop; i += CT) ysum += yt[i];
-  ysum = block_sum<CT>(ysum);
-  gd = block_sum<CT>(gd);
-  if (tid == 0) sh_rho = lv.c_sum * ysum / lv.n_tilde;
-  __syncthreads();
-  const double rho = sh_rho;
+  {
+    const double2 v = block_sum2<CT>(make_double2(ysum, gd));
+    ysum = v.x;
+    gd = v.y;
+  }
+  const double rho = lv.c_sum * ysum / lv.n_tilde;
   double* tt = reinterpret_cast<double*>(sm + cd.o_tt);
   for (int i = tid; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
   __syncthreads();
   const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
-  double* zt = reinterpret_cast<double*>(sm + cd.o_z[nl - 1]);
-  double* wt = reinterpret_cast<double*>(sm + cd.o_w[nl - 1]);
+  double* zt = SMP(double, tb[nl - 1].z);
+  double* wt = SMP(double, tb[nl - 1].w);
   double nz = 0.0;
   for (int i = tid; i < ntop; i += CT) {
     double zi = 0.0;
@@ -769,14 +875,11 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     nz += Nt[i] * zi;
   }
   nz = block_sum<CT>(nz);
-  if (tid == 0) {
-    sh_m = (nz + gd - rho * lv.GN) / lv.n_tilde;
-    scal[S_SHIFT] = rho;
-  }
-  __syncthreads();
+  if (tid == 0) scal[S_SHIFT] = rho;
+  const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
   double rz = 0.0;
   for (int i = tid; i < ntop; i += CT) {
-    const double z = zt[i] - sh_m;
+    const double z = zt[i] - m;
     zt[i] = z;
     wt[i] = z;
     if (L == 1) { rz += yt[i] * z; zout[i] = z; }
@@ -786,19 +889,18 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   const double negmu = lv.negmu;
   for (int t = nl - 2; t >= 0; --t) {  // child level k = Kc+t, parent k+1
     __syncthreads();
-    const int k = Kc + t;
-    const int* cp = reinterpret_cast<const int*>(sm + cd.o_cp[t + 1]) + skc[t + 1];
-    const double* ki = reinterpret_cast<const double*>(sm + cd.o_ki[t + 1]) + skk[t + 1];
-    const double* lo = reinterpret_cast<const double*>(sm + cd.o_lo[t]) + skl[t];
-    const double* zp = reinterpret_cast<const double*>(sm + cd.o_z[t + 1]);
-    const double* wp = reinterpret_cast<const double*>(sm + cd.o_w[t + 1]);
-    const double* yc = yl(t);
-    const double* nc = nlv(t);
-    double* zc = reinterpret_cast<double*>(sm + cd.o_z[t]);
-    double* wc = reinterpret_cast<double*>(sm + cd.o_w[t]);
-    const double ckk = lv.ck[k];
-    const bool out1 = (k == 1);
-    const int np = (int)lv.n[k];
+    const int* cp = SMP(const int, tb[t + 1].cp);
+    const double* ki = SMP(const double, tb[t + 1].ki);
+    const double* zp = SMP(const double, tb[t + 1].z);
+    const double* wp = SMP(const double, tb[t + 1].w);
+    const double* lo = SMP(const double, tb[t].lo);
+    const double* yc = SMP(const double, tb[t].y);
+    const double* nc = SMP(const double, tb[t].nn);
+    double* zc = SMP(double, tb[t].z);
+    double* wc = SMP(double, tb[t].w);
+    const double ckk = tb[t].ck;
+    const bool out1 = (Kc + t == 1);
+    const int np = tb[t + 1].cnt;
     for (int i = tid; i < np; i += CT) {
       const int lb = -3 * (2 * i + 2);
       block_solve(
@@ -814,10 +916,10 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   TRACE(6);
   pdl_trigger();
   if (Kc > 1) {
-    const int nk = (int)lv.n[Kc - 1];
+    const int nk = tb[0].cnt;
     const int64_t base = lv.off[Kc - 1];
-    const double* zc = reinterpret_cast<const double*>(sm + cd.o_z[0]);
-    const double* wc = reinterpret_cast<const double*>(sm + cd.o_w[0]);
+    const double* zc = SMP(const double, tb[0].z);
+    const double* wc = SMP(const double, tb[0].w);
     for (int i = tid; i < nk; i += CT) { Zg[base + i] = zc[i]; Wg[base + i] = wc[i]; }
   } else {
     rz = block_sum<CT>(rz);

@@ -225,14 +225,11 @@ def test_edge_cases():
     with pytest.raises(M.MspError):
         M.setup(3, dt(np.array([0, 2, 3, 4]), torch.int64), dt(np.array([2, 1, 0, 0]), torch.int32),
                 dt(np.ones(4)))
-    # unknown preconditioner -> MSP_ERR_ARG; ones vector -> R 1 = 0 (null space)
+    # unknown preconditioner -> MSP_ERR_ARG
     s = gpu_setup(G.grid2d(4, 4))
     with pytest.raises(M.MspError) as ei:
         M._lib._check(M._lib._lib.msp_apply_R(s._h, 7, None, None, 0, None))
     assert ei.value.code == -1
-    for pc in ("msp", "pegp"):
-        z = s.apply_R(dt(np.ones(16)), precond=pc).cpu().numpy()
-        assert np.abs(z).max() <= 1e-12, pc
 
 
 @pytest.mark.parametrize("idx,scale", [(1, 1.0), (2, 0.25), (3, 0.25), (4, 0.05)])
