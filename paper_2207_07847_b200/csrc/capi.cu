@@ -101,6 +101,7 @@ int msp_setup(int64_t n, const int64_t* rowptr, const int32_t* col, const double
       msp::validate_csr(h, drp, dcol, dw, st);
       msp::build_setup(h, drp, dcol, dw, st);
       msp::alloc_solve_workspace(h);
+      msp::build_coarse_matrix(h, st);
       MSP_CUDA(cudaStreamSynchronize(st));
     } catch (...) {
       delete H;

@@ -135,6 +135,10 @@ struct Handle {
   int32_t Kc = 1;
   size_t coarse_smem = 0;
   CoarseDesc cdesc{};
+  // coarse levels Kc..L as a dense map:
+  // [z_Kc; w_Kc] = Mco [y_Kc; gdot], row-major (2 n_Kc) x (n_Kc + 1)
+  bool gemv = false;
+  DBuf<double> Mco;
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
 
@@ -204,5 +208,6 @@ void expanded_to_nested(Handle& h, const double* src, double* dst, cudaStream_t 
 void nested_to_expanded(Handle& h, const double* src, double* dst, cudaStream_t st);
 Lv make_level_table(const Handle& h);              // setup.cu
 void release_graph(Handle& h);
+void build_coarse_matrix(Handle& h, cudaStream_t st);  // solve.cu
 
 }  // namespace msp

@@ -39,6 +39,8 @@ struct TierDesc {
   int o_n[MAXT];   // N of level k0+t: t = 0 staged (k0 > 1), 1..nl-2 computed
   int o_z[MAXT];   // z, w of level k0+t: t = nl-1 staged, 1..nl-2 computed
   int o_w[MAXT];
+  int o_v;         // GEMV input [y_Kc; gdot] (top tier in GEMV mode), -1 otherwise
+  int gemv_n;      // n_Kc when this tier's down kernel forms z, w at Kc by the GEMV
   int smem_down;
   // up kernel (its own layout): first level-k0 descendant of each level-k1
   // node of the tile (int32, [a, b]) and y at level k0

@@ -884,11 +884,13 @@ inline int a16(int64_t b) { return (int)((b + 15) & ~(int64_t)15); }
 // cap[t] (nodes) and caplo[t] (leftovers among level-(k0+t) children);
 // the up kernel's segments come first (smem_up is their end)
 TierDesc tier_layout(int k0, int nl, int64_t ntiles, const std::vector<int64_t>& cap,
-                     const std::vector<int64_t>& caplo) {
+                     const std::vector<int64_t>& caplo, int64_t gemv_n) {
   TierDesc d{};
   d.k0 = k0;
   d.nl = nl;
   d.ntiles = (int)ntiles;
+  d.gemv_n = (int)gemv_n;
+  d.o_v = -1;
   int64_t cur = 0;
   auto take = [&](int64_t bytes) { const int o = a16(cur); cur = o + bytes; return o; };
   d.o_uf = take((cap[nl - 1] + 1 + 8) * 4);
@@ -908,6 +910,7 @@ TierDesc tier_layout(int k0, int nl, int64_t ntiles, const std::vector<int64_t>&
   }
   d.o_z[nl - 1] = take((cap[nl - 1] + 2) * 8);
   d.o_w[nl - 1] = take((cap[nl - 1] + 2) * 8);
+  if (gemv_n > 0) d.o_v = take((gemv_n + 1) * 8);
   d.smem_down = a16(cur);
   return d;
 }
@@ -958,6 +961,9 @@ void build_schedule(Handle& h, cudaStream_t st) {
   const Lv lv = make_level_table(h);
 
   // coarse level: smallest Kc whose levels Kc..L fit the single-CTA kernel
+  // (and, in GEMV mode, whose n_Kc <= GEMV_MAX)
+  int64_t GEMV_MAX = 0;  // off: see DESIGN.md "Coarse GEMV" (3e-12 vs 1e-14 accuracy, no faster)
+  if (const char* e = std::getenv("MSP_GEMV_MAX")) GEMV_MAX = std::atoll(e);
   const bool stage_pinv = h.lv[L - 1].n <= 32;
   {
     int Kc = L;
@@ -966,10 +972,13 @@ void build_schedule(Handle& h, cudaStream_t st) {
       tail += h.lv[k - 1].n;
       if (tail > CMAX || L - k + 1 > MAXT + 8) break;
       if ((size_t)coarse_desc(h, k, stage_pinv).smem > SMEM_CAP) break;
+      if (GEMV_MAX > 0 && k > 1 && h.lv[k - 1].n > GEMV_MAX) break;
       Kc = k;
     }
     h.Kc = Kc;
   }
+  // GEMV mode needs Kc > 1 and a tiled top tier (checked below)
+  bool gemv_ok = GEMV_MAX > 0 && h.Kc > 1;
   h.cdesc = coarse_desc(h, h.Kc, stage_pinv);
   h.coarse_smem = (size_t)h.cdesc.smem;
 
@@ -1020,7 +1029,8 @@ void build_schedule(Handle& h, cudaStream_t st) {
           }
         }
       }
-      t.desc = tier_layout(k0_, nl, t.ntiles, cap, caplo);
+      const bool top = (k1_ == h.Kc) && gemv_ok;
+      t.desc = tier_layout(k0_, nl, t.ntiles, cap, caplo, top ? h.lv[h.Kc - 1].n : 0);
       const int64_t nk1 = h.lv[k1_ - 1].n;
       t.firstk0.alloc(nk1 + 1 + 8);
       MSP_CUDA(cudaMemsetAsync(t.firstk0.p, 0, (nk1 + 1 + 8) * sizeof(int32_t), st));
@@ -1080,6 +1090,8 @@ void build_schedule(Handle& h, cudaStream_t st) {
       throw Error{MSP_ERR_UNSUPPORTED, "a tile does not fit in shared memory"};
     k0 = k1;
   }
+  h.gemv = gemv_ok && !h.tiers.empty() && !h.tiers.back().generic && h.tiers.back().k1 == h.Kc &&
+           h.tiers.back().desc.gemv_n > 0;
 }
 
 }  // namespace msp

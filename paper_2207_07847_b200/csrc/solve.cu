@@ -51,7 +51,7 @@ enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S
 // counter slots
 enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
 // sweep modes
-enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2 };
+enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2, M_COLUMN = 3 };
 
 // phase timestamps for kernel-structure work (build with -DMSP_TRACE; the
 // in-tree library never defines it)
@@ -519,12 +519,14 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
                                                   const double* __restrict__ Nsub, const double* __restrict__ y0src,
                                                   double* __restrict__ Zg, double* __restrict__ Wg,
                                                   double* __restrict__ zout, double* __restrict__ part,
-                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
+                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode,
+                                                  const double* __restrict__ Mco, const double* __restrict__ part_gd,
+                                                  int npart_gd, const double* __restrict__ Ygl) {
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int sa[MAXT], sn[MAXT], skc[MAXT], skk[MAXT], skl[MAXT];
   __shared__ int sky0, skn0, skz, skw, sdone;
-  __shared__ double srho;
+  __shared__ double srho, srho_g;
   __shared__ LvlPtr tb[MAXT];
   const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x;
@@ -569,18 +571,58 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
     srho = scal[S_SHIFT];
   }
+  const bool gemv = td.gemv_n > 0;
   if (g == 3 * m1 + 1) {
     const int64_t base = FIRST ? 0 : lv.off[k0 - 1];
     sky0 = stage_window(&bar, sm + td.o_y[0], y0src, 8, base + sa[0], base + sa[0] + sn[0]);
-  } else if (g == 3 * m1 + 2 || g == 3 * m1 + 3) {
+  } else if (!gemv && (g == 3 * m1 + 2 || g == 3 * m1 + 3)) {
     const bool isz = (g == 3 * m1 + 2);
     const int64_t base = lv.off[k0 + nl - 2] + sa[nl - 1];
     const int v = stage_window(&bar, sm + (isz ? td.o_z[nl - 1] : td.o_w[nl - 1]), isz ? Zg : Wg, 8, base,
                                base + sn[nl - 1]);
     if (isz) skz = v; else skw = v;
   }
+  if (gemv) {
+    // Coarse GEMV (levels Kc..L folded into a dense map at setup): z, w of
+    // this tile's level-Kc nodes = Mco [y_Kc; gdot]; rho from the same y_Kc
+    const int nk = td.gemv_n;
+    double* v = reinterpret_cast<double*>(sm + td.o_v);
+    const int64_t okc = lv.off[k0 + nl - 2];
+    double ys = 0.0, gd = 0.0;
+    for (int j = tid; j < nk; j += TT) {
+      const double yv = __ldcg(Ygl + okc + j);
+      v[j] = yv;
+      ys += yv;
+    }
+    for (int j = tid; j < npart_gd; j += TT) gd += __ldcg(part_gd + j);
+    const double2 sums = block_sum2<TT>(make_double2(ys, gd));
+    if (tid == 0) {
+      v[nk] = sums.y;
+      srho_g = lv.c_sum * sums.x / lv.n_tilde;
+      skz = 0;
+      skw = 0;
+    }
+    __syncthreads();
+    // warp per output row: rows [a, a+cnt) of z then of w
+    const int a = sa[nl - 1], cnt = sn[nl - 1], lane = tid & 31, warp = tid >> 5;
+    double* zt = reinterpret_cast<double*>(sm + td.o_z[nl - 1]);
+    double* wt = reinterpret_cast<double*>(sm + td.o_w[nl - 1]);
+    for (int rr = warp; rr < 2 * cnt; rr += TT / 32) {
+      const int row = (rr < cnt) ? a + rr : nk + a + (rr - cnt);
+      const double* Mr = Mco + (int64_t)row * (nk + 1);
+      double acc = 0.0;
+      for (int j = lane; j <= nk; j += 32) acc += Mr[j] * v[j];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (rr < cnt) zt[rr] = acc;
+        else wt[rr - cnt] = acc;
+      }
+    }
+    if (tid == 0 && blockIdx.x == 0 && mode != M_COLUMN) scal[S_SHIFT] = srho_g;
+  }
   __syncthreads();
   const int done = sdone;
+  if (gemv && tid == 0) srho = srho_g;
   if (tid == 0) mbar_arrive(&bar);
   mbar_wait(&bar, 0);
   TRACE(3);
@@ -803,18 +845,23 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   TRACE(1);
   pdl_wait();
   TRACE(2);
-  if (tid == 0) sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+  if (tid == 0) sdone = (mode == M_INIT || mode == M_ITER) ? (int)cnt[C_DONE] : 0;
   __syncthreads();
   const int done = sdone;
   if (g == 3 * m1 + nl + 1 && !done) {
-    const int64_t base = (Kc == 1) ? 0 : lv.off[Kc - 1];
+    // M_COLUMN (setup of the coarse GEMV matrix): CTA j solves for the j-th
+    // unit input, whose y_Kc is row j of y0src (n_Kc x n_Kc identity, then 0)
+    const int64_t base = (mode == M_COLUMN) ? (int64_t)blockIdx.x * lv.n[Kc - 1] : ((Kc == 1) ? 0 : lv.off[Kc - 1]);
     sky0 = stage_window(&bar, sm + cd.o_y[0], y0src, 8, base, base + lv.n[Kc - 1]);
   }
   __syncthreads();
   if (tid == 0) mbar_arrive(&bar);
   double gd = 0.0;
-  if (!done)
+  if (mode == M_COLUMN) {
+    if (tid == 0) gd = ((int64_t)blockIdx.x == lv.n[Kc - 1]) ? 1.0 : 0.0;
+  } else if (!done) {
     for (int i = tid; i < npart; i += CT) gd += __ldcg(part_gd + i);
+  }
   mbar_wait(&bar, 0);
   TRACE(3);
   if (done) return;
@@ -875,7 +922,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     nz += Nt[i] * zi;
   }
   nz = block_sum<CT>(nz);
-  if (tid == 0) scal[S_SHIFT] = rho;
+  if (tid == 0 && mode != M_COLUMN) scal[S_SHIFT] = rho;
   const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
   double rz = 0.0;
   for (int i = tid; i < ntop; i += CT) {
@@ -915,7 +962,13 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   __syncthreads();
   TRACE(6);
   pdl_trigger();
-  if (Kc > 1) {
+  if (mode == M_COLUMN) {  // column j of the GEMV matrix: [z_Kc; w_Kc]
+    const int nk = tb[0].cnt;
+    double* col = Zg + (int64_t)blockIdx.x * 2 * nk;
+    const double* zc = SMP(const double, tb[0].z);
+    const double* wc = SMP(const double, tb[0].w);
+    for (int i = tid; i < nk; i += CT) { col[i] = zc[i]; col[nk + i] = wc[i]; }
+  } else if (Kc > 1) {
     const int nk = tb[0].cnt;
     const int64_t base = lv.off[Kc - 1];
     const double* zc = SMP(const double, tb[0].z);
@@ -1074,8 +1127,8 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     }
     ++h.launches;
   }
-  // ---- coarse
-  {
+  // ---- coarse (folded into the top tier's down kernel in GEMV mode)
+  if (!h.gemv) {
     P.begin();
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
     launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
@@ -1108,12 +1161,14 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
         launch(k_tile_down<true>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
-               cnt, mode);
+               cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, (int)h.tiers[0].ntiles,
+               (const double*)h.Y.p);
       else
         launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
-               scal, cnt, mode);
+               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, (int)h.tiers[0].ntiles,
+               (const double*)h.Y.p);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
@@ -1152,6 +1207,37 @@ void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t
 }
 
 }  // namespace
+
+// The coarse levels Kc..L map (y_Kc, gdot) linearly to (z_Kc, w_Kc): run the
+// coarse kernel once per unit input (n_Kc + 1 CTAs) and keep the map as a
+// dense row-major matrix for the GEMV in the top tier's down kernel.
+__global__ void k_unit_rows(int64_t nk, double* __restrict__ E) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < (nk + 1) * nk) E[i] = ((i / nk) == (i % nk)) ? 1.0 : 0.0;
+}
+
+__global__ void k_transpose(int64_t rows, int64_t cols, const double* __restrict__ C, double* __restrict__ M) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // i = r * cols + c of M
+  if (i < rows * cols) M[i] = C[(i % cols) * rows + (i / cols)];
+}
+
+void build_coarse_matrix(Handle& h, cudaStream_t st) {
+  if (!h.gemv) return;
+  const int64_t nk = h.lv[h.Kc - 1].n;
+  DBuf<double> E, C;
+  E.alloc((nk + 1) * nk + 8);
+  C.alloc(2 * nk * (nk + 1) + 8);
+  h.Mco.alloc(2 * nk * (nk + 1) + 8);
+  k_unit_rows<<<grid_for((nk + 1) * nk), TPB, 0, st>>>(nk, E.p);
+  const Lv lv = make_level_table(h);
+  launch(k_coarse, (unsigned)(nk + 1), CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
+         (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
+         (const double*)E.p, C.p, C.p, (double*)nullptr, (const double*)nullptr, 0, h.scal.p, h.counters.p,
+         (int)M_COLUMN);
+  k_transpose<<<grid_for(2 * nk * (nk + 1)), TPB, 0, st>>>(2 * nk, nk + 1, C.p, h.Mco.p);
+  MSP_LAUNCH_CHECK();
+  MSP_CUDA(cudaStreamSynchronize(st));
+}
 
 void release_graph(Handle& h) {
   if (h.graph) cudaGraphExecDestroy(h.graph);

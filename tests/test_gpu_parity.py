@@ -53,6 +53,9 @@ GRAPHS = {
     "paper_fig2": G.paper_example_8,
     "path_3": lambda: G.from_edges(3, [0, 1], [1, 2], [1.0, 2.0]),
     "star_40": lambda: G.from_edges(41, np.zeros(40, int), np.arange(1, 41), np.linspace(1, 2, 40)),
+    # large enough for tiers + the coarse GEMV (n_Kc <= 512 below a tiled top tier)
+    "grid_90x70_loguniform": lambda: G.grid2d(90, 70, "loguniform", 8),
+    "rgg_12000": lambda: G.rgg(12000, 12.0, 2),
 }
 
 
