@@ -337,6 +337,33 @@ int msp_solve_LH(msp_handle* H, const double* r, double* z, int mem, void* strea
   });
 }
 
+int msp_dist_solve(msp_handle* H, const msp_comm* comm, const double* b, double* x, double rtol, int32_t maxit,
+                   int mem, void* stream, msp_report* rep) {
+  return guarded([&] {
+    need(H && comm && b && x, "null argument");
+    need(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world, "bad rank / world");
+    need(comm->allreduce && comm->allgather && comm->alltoallv, "missing communication callback");
+    need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
+    need(rtol >= 0 && maxit >= 0, "bad rtol / maxit");
+    Handle& h = H->h;
+    cudaStream_t st = S(stream);
+    const double* bd = stage_in(h, b, mem, h.stage_in, st);
+    msp::gather_to_nested(h, bd, h.vb.p, st);
+    msp::pcg_dist_nested(h, *comm, h.vb.p, h.vx.p, rtol, maxit, st, rep);
+    // keep own rows only (the rest of vx is stale): zero elsewhere
+    msp::zero_outside(h, h.vx.p, st);
+    if (mem == MSP_MEM_DEVICE) {
+      msp::scatter_from_nested(h, h.vx.p, x, st);
+      MSP_CUDA(cudaStreamSynchronize(st));
+    } else {
+      if (h.stage_out.n < (size_t)h.n) h.stage_out.alloc(h.n);
+      msp::scatter_from_nested(h, h.vx.p, h.stage_out.p, st);
+      MSP_CUDA(cudaMemcpyAsync(x, h.stage_out.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+    }
+  });
+}
+
 int msp_set_profiling(msp_handle* H, int on) {
   return guarded([&] {
     need(H != nullptr, "null handle");

@@ -154,6 +154,7 @@ struct Handle {
   double pegp_rtol = 1e-13;
   int pegp_maxit = 5000;
   int pegp_last_inner = 0;
+  int64_t dist_row0 = 0, dist_row1 = 0;  // own rows of the last msp_dist_solve
 
   // ---- solve workspaces
   DBuf<double> Y, Z, W;       // n~-layout sweep vectors (y = P^T sums, z, w)
@@ -196,6 +197,9 @@ void gather_to_nested(Handle& h, const double* src_orig, double* dst_nested, cud
 void scatter_from_nested(Handle& h, const double* src_nested, double* dst_orig, cudaStream_t st);
 void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol, int maxit,
                 cudaStream_t st, msp_report* rep);
+void zero_outside(Handle& h, double* x, cudaStream_t st);
+void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x, double rtol, int maxit,
+                     cudaStream_t st, msp_report* rep);
 void alloc_solve_workspace(Handle& h);
 void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
 // pegp.cu

@@ -47,11 +47,13 @@ constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 constexpr int CT = MSP_CT;    // coarse kernel (single CTA)
 
 // device scalar slots
-enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S_NSCAL };
+enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_GD, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S_RZ, S_NSCAL };
 // counter slots
 enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
 // sweep modes
 enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2, M_COLUMN = 3 };
+// multi-GPU: local totals only (the caller all-reduces, k_dist_finish derives)
+constexpr int M_DIST = 16;
 
 // phase timestamps for kernel-structure work (build with -DMSP_TRACE; the
 // in-tree library never defines it)
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
                                               const double* __restrict__ pold, double* __restrict__ pnew,
                                               double* __restrict__ q, double* __restrict__ x,
                                               double* __restrict__ part, double* __restrict__ scal,
-                                              unsigned int* __restrict__ cnt) {
+                                              unsigned int* __restrict__ cnt, int64_t row0, int64_t row1) {
   pdl_wait();
   if (PCG && cnt[C_DONE]) return;
   const double beta = PCG ? scal[S_BETA] : 0.0;
@@ -292,9 +294,10 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
   const int64_t warp = (blockIdx.x * (int64_t)TPB + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * TPB) >> 5;
   double d = 0.0;
-  for (int64_t s = warp; s < nslices; s += nwarps) {
+  const int64_t s_begin = row0 >> 5, s_end = (row1 + 31) >> 5;
+  for (int64_t s = s_begin + warp; s < s_end; s += nwarps) {
     const int64_t r = s * 32 + lane;
-    const bool valid = r < n;
+    const bool valid = r < n && r >= row0 && r < row1;
     const bool lng = (smask[s] >> lane) & 1u;
     const int64_t base = sptr[s];
     const int width = (int)((sptr[s + 1] - base) >> 5);
@@ -322,6 +325,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
   }
   for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
     const int64_t r = long_rows[i];
+    if (r < row0 || r >= row1) continue;
     const double po = PCG ? pold[r] : 0.0;
     const double pi = PCG ? z[r] + beta * po : z[r];
     double acc = 0.0;
@@ -414,11 +418,14 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
                                                 const double* __restrict__ q, double* __restrict__ r,
                                                 const double* __restrict__ H, double* __restrict__ Yg,
                                                 double* __restrict__ part_rr, double* __restrict__ part_gd,
-                                                double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
+                                                double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode_in,
+                                                int tile0) {
+  const int mode = mode_in & 15;
+  const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone;
-  const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -496,8 +503,11 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
       if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
-        const double tot = warp_sum_partials(part_rr, gridDim.x);
-        if (tid == 0) {
+        const double tot = warp_sum_partials(part_rr + tile0, gridDim.x);
+        if (dist) {  // local totals; k_dist_finish runs after the all-reduce
+          const double tgd = warp_sum_partials(part_gd + tile0, gridDim.x);
+          if (tid == 0) { scal[S_RR] = tot; scal[S_GD] = tgd; cnt[C_UPD] = 0; }
+        } else if (tid == 0) {
           finish_rr(tot, scal, cnt, mode);
           cnt[C_UPD] = 0;
         }
@@ -519,16 +529,18 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
                                                   const double* __restrict__ Nsub, const double* __restrict__ y0src,
                                                   double* __restrict__ Zg, double* __restrict__ Wg,
                                                   double* __restrict__ zout, double* __restrict__ part,
-                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode,
+                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode_in,
                                                   const double* __restrict__ Mco, const double* __restrict__ part_gd,
-                                                  int npart_gd, const double* __restrict__ Ygl) {
+                                                  int npart_gd, const double* __restrict__ Ygl, int tile0) {
+  const int mode = mode_in & 15;
+  const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int sa[MAXT], sn[MAXT], skc[MAXT], skk[MAXT], skl[MAXT];
   __shared__ int sky0, skn0, skz, skw, sdone;
   __shared__ double srho, srho_g;
   __shared__ LvlPtr tb[MAXT];
-  const int tile = blockIdx.x, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   TRACE(0);
@@ -728,8 +740,12 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) part[tile] = rz;
       if (mode != M_APPLY && warp_last_block(&cnt[C_DOWN])) {
-        const double tot = warp_sum_partials(part, gridDim.x);
-        if (tid == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+        const double tot = warp_sum_partials(part + tile0, gridDim.x);
+        if (tid == 0) {
+          if (dist) scal[S_RZ] = tot;
+          else finish_rz(tot, scal, mode);
+          cnt[C_DOWN] = 0;
+        }
       }
     }
   }
@@ -805,7 +821,9 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
                                                double* __restrict__ Zg, double* __restrict__ Wg,
                                                double* __restrict__ zout, const double* __restrict__ part_gd,
                                                int npart, double* __restrict__ scal, unsigned int* __restrict__ cnt,
-                                               int mode) {
+                                               int mode_in) {
+  const int mode = mode_in & 15;
+  const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
@@ -859,6 +877,8 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   double gd = 0.0;
   if (mode == M_COLUMN) {
     if (tid == 0) gd = ((int64_t)blockIdx.x == lv.n[Kc - 1]) ? 1.0 : 0.0;
+  } else if (dist) {
+    if (tid == 0) gd = scal[S_GD];  // all-reduced by the caller
   } else if (!done) {
     for (int i = tid; i < npart; i += CT) gd += __ldcg(part_gd + i);
   }
@@ -1097,7 +1117,118 @@ struct Prof {
 
 // R r (MSP) on nested vectors.  mode APPLY: r -> z;  INIT / ITER: the PCG
 // step (ITER first updates r) with the scalars of reading R10.
-void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P) {
+// ----------------------------------------------------------- multi-GPU
+// State of one rank of the partitioned solve (msp_dist_solve).
+struct DistCtx {
+  msp_comm comm;
+  int64_t row0 = 0, row1 = 0, tile0 = 0, tile1 = 0;
+  int64_t k1 = 0, k1lo = 0, k1hi = 0, k1max = 0;  // first tier's top level, own range, largest range
+  std::vector<int64_t> send_counts, recv_counts;
+  DBuf<int32_t> send_idx, recv_idx;
+  DBuf<double> sendbuf, recvbuf, gbuf_send, gbuf_recv;
+  std::vector<int64_t> k1lo_all;
+};
+
+void comm_check(int rc, const char* what) {
+  if (rc != 0) throw Error{MSP_ERR_CUDA, std::string("communication callback failed: ") + what};
+}
+
+__global__ void k_dist_finish(int stage, double* scal, unsigned int* cnt, int mode) {
+  if (stage == 0) {
+    scal[S_ALPHA] = scal[S_RHO] / scal[S_PQ];
+  } else if (stage == 1) {
+    finish_rr(scal[S_RR], scal, cnt, mode);
+  } else if (!cnt[C_DONE] || mode == M_INIT) {
+    finish_rz(scal[S_RZ], scal, mode);
+  }
+}
+
+// own rows: x += alpha p_old (deferred), p = z + beta p_old (in place)
+__global__ void k_dist_p(int64_t row0, int64_t row1, const double* __restrict__ z, double* __restrict__ p,
+                         double* __restrict__ x, const double* __restrict__ scal, const unsigned* __restrict__ cnt) {
+  if (cnt[C_DONE]) return;
+  const double beta = scal[S_BETA], alpha = scal[S_ALPHA];
+  for (int64_t i = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row1; i += (int64_t)gridDim.x * blockDim.x) {
+    const double po = p[i];
+    x[i] += alpha * po;
+    p[i] = z[i] + beta * po;
+  }
+}
+
+__global__ void k_take(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) dst[k] = src[idx[k]];
+}
+
+__global__ void k_put(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) dst[idx[k]] = src[k];
+}
+
+// local (a, b) over [row0, row1) into scal[slot] (fixed order)
+__global__ void __launch_bounds__(TPB) k_dot_rows(int64_t row0, int64_t row1, const double* __restrict__ a,
+                                                  const double* __restrict__ b, double* __restrict__ part,
+                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int slot) {
+  double d = 0.0;
+  for (int64_t i = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row1; i += (int64_t)gridDim.x * blockDim.x)
+    d += a[i] * b[i];
+  d = block_sum<TPB>(d);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) part[blockIdx.x] = d;
+    if (warp_last_block(&cnt[C_SPMV])) {
+      const double t = warp_sum_partials(part, gridDim.x);
+      if (threadIdx.x == 0) { scal[slot] = t; cnt[C_SPMV] = 0; }
+    }
+  }
+}
+
+__global__ void k_pack(int64_t n, const double* __restrict__ src, double* __restrict__ dst, int64_t m) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) dst[i] = (i < n) ? src[i] : 0.0;
+}
+
+bool read_done(Handle& h, cudaStream_t st) {
+  unsigned c[C_NCNT];
+  MSP_CUDA(cudaMemcpyAsync(c, h.counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+  MSP_CUDA(cudaStreamSynchronize(st));
+  return c[C_DONE] != 0;
+}
+
+// after the first tier's up kernel: all-reduce ((r, r), gdot), convergence
+// test, all-gather y at level k1.  false: converged (stop the sweep).
+bool dist_after_tier1_up(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
+  if (mode != M_APPLY) {
+    comm_check(d.comm.allreduce(h.scal.p + S_RR, 2, d.comm.ctx), "allreduce(rr, gdot)");
+    k_dist_finish<<<1, 1, 0, st>>>(1, h.scal.p, h.counters.p, mode);
+    MSP_LAUNCH_CHECK();
+    h.launches += 1;
+    if (read_done(h, st)) return false;
+  }
+  const int64_t off = h.lv[d.k1 - 1].off;
+  const int64_t m = d.k1max;
+  k_pack<<<grid_for(m), TPB, 0, st>>>(d.k1hi - d.k1lo, h.Y.p + off + d.k1lo, d.gbuf_send.p, m);
+  MSP_LAUNCH_CHECK();
+  comm_check(d.comm.allgather(d.gbuf_send.p, d.gbuf_recv.p, m, d.comm.ctx), "allgather(y_k1)");
+  for (int q = 0; q < d.comm.world; ++q) {
+    const int64_t lo = d.k1lo_all[q], cnt = d.k1lo_all[q + 1] - lo;
+    if (cnt > 0)
+      MSP_CUDA(cudaMemcpyAsync(h.Y.p + off + lo, d.gbuf_recv.p + (int64_t)q * m, cnt * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+  }
+  h.launches += 1;
+  return true;
+}
+
+void dist_after_tier1_down(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
+  if (mode == M_APPLY) return;
+  comm_check(d.comm.allreduce(h.scal.p + S_RZ, 1, d.comm.ctx), "allreduce(rz)");
+  k_dist_finish<<<1, 1, 0, st>>>(2, h.scal.p, h.counters.p, mode);
+  MSP_LAUNCH_CHECK();
+  h.launches += 1;
+}
+
+void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P,
+                DistCtx* dc = nullptr) {
   double* part_rr = h.red.p;                  // [cap/4]
   double* part_rz = h.red.p + h.red_cap / 4;
   double* part_gd = h.red.p + h.red_cap / 2;
@@ -1116,16 +1247,17 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(PC_MID_UP);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_up<true>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.desc,
-               (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
-               part_rr, part_gd, scal, cnt, mode);
+        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : T.ntiles), TT, T.smem_up, st, lv,
+               T.desc, (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p,
+               h.Y.p, part_rr, part_gd, scal, cnt, mode | (dc ? M_DIST : 0), (int)(dc ? dc->tile0 : 0));
       else
         launch(k_tile_up<false>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
-               part_rr, part_gd, scal, cnt, mode);
+               part_rr, part_gd, scal, cnt, mode, 0);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
     }
     ++h.launches;
+    if (dc && i == 0 && !dist_after_tier1_up(h, *dc, st, mode)) return;  // converged
   }
   // ---- coarse (folded into the top tier's down kernel in GEMV mode)
   if (!h.gemv) {
@@ -1133,7 +1265,8 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
     launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
            (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
-           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int)h.tiers[0].ntiles, scal, cnt, mode);
+           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int)h.tiers[0].ntiles, scal, cnt,
+           mode | (dc ? M_DIST : 0));
     P.end(PC_COARSE);
     ++h.launches;
   }
@@ -1158,21 +1291,23 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_down<true>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
+        launch(k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : T.ntiles), TT, T.smem_down, st, lv,
+               T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
-               cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, (int)h.tiers[0].ntiles,
-               (const double*)h.Y.p);
+               cnt, mode | (dc ? M_DIST : 0), (const double*)h.Mco.p, (const double*)part_gd,
+               (int)h.tiers[0].ntiles, (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0));
       else
         launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, (int)h.tiers[0].ntiles,
-               (const double*)h.Y.p);
+               (const double*)h.Y.p, 0);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
   }
+  if (dc) dist_after_tier1_down(h, *dc, st, mode);
 }
 
 template <bool PCG>
@@ -1181,7 +1316,7 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
   launch(k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
          (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
          (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
-         (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p);
+         (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, (int64_t)0, h.n);
   ++h.launches;
 }
 
@@ -1439,3 +1574,144 @@ extern "C" int msp_debug_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, msp::g_trace, sizeof(msp::g_trace)) == cudaSuccess ? 0 : -2;
 }
 #endif
+
+namespace msp {
+
+// One rank of the partitioned PCG-MSP solve (msp_dist_solve), nested vectors.
+void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x, double rtol, int maxit,
+                     cudaStream_t st, msp_report* rep) {
+  if (h.tiers.empty() || h.tiers[0].generic || h.tiers[0].k1 < 2 || h.Kc < 2)
+    throw Error{MSP_ERR_UNSUPPORTED, "multi-GPU solve needs a tiled first tier (graph too small or too irregular)"};
+  const Handle::Tier& T1 = h.tiers[0];
+  DistCtx d;
+  d.comm = comm;
+  const int W = comm.world, R = comm.rank;
+  // ---- plan (host): level-1 CSR and first-tier tile starts to the host
+  std::vector<int32_t> rp(h.n + 1), cl(h.nnz_adj), ts((size_t)(T1.k1 - T1.k0 + 1) * (T1.ntiles + 1));
+  MSP_CUDA(cudaMemcpy(rp.data(), h.rowptr1.p, rp.size() * 4, cudaMemcpyDeviceToHost));
+  MSP_CUDA(cudaMemcpy(cl.data(), h.col1.p, cl.size() * 4, cudaMemcpyDeviceToHost));
+  MSP_CUDA(cudaMemcpy(ts.data(), T1.tstart.p, ts.size() * 4, cudaMemcpyDeviceToHost));
+  const int64_t nt1 = T1.ntiles + 1;
+  int64_t range[4];
+  d.send_counts.assign(W, 0);
+  d.recv_counts.assign(W, 0);
+  int rc = msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, R, range, d.recv_counts.data(),
+                              d.send_counts.data(), nullptr, 0, nullptr, 0);
+  if (rc) throw Error{rc, "partition plan"};
+  int64_t nrecv = 0, nsend = 0;
+  for (int q = 0; q < W; ++q) { nrecv += d.recv_counts[q]; nsend += d.send_counts[q]; }
+  std::vector<int64_t> rr(std::max<int64_t>(nrecv, 1)), sr(std::max<int64_t>(nsend, 1));
+  rc = msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, R, range, d.recv_counts.data(),
+                          d.send_counts.data(), rr.data(), nrecv, sr.data(), nsend);
+  if (rc) throw Error{rc, "partition plan"};
+  d.row0 = range[0]; d.row1 = range[1]; d.tile0 = range[2]; d.tile1 = range[3];
+  d.k1 = T1.k1;
+  const int64_t top = (int64_t)(T1.k1 - T1.k0) * nt1;
+  d.k1lo_all.assign(W + 1, 0);
+  for (int q = 0; q <= W; ++q) {
+    // rank q's tile range, recomputed with the same rule
+    int64_t rq[4];
+    std::vector<int64_t> dummy(W);
+    if (q < W) {
+      msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, q, rq, dummy.data(), dummy.data(),
+                         nullptr, 0, nullptr, 0);
+      d.k1lo_all[q] = ts[top + rq[2]];
+    } else {
+      d.k1lo_all[q] = ts[top + T1.ntiles];
+    }
+  }
+  d.k1lo = d.k1lo_all[R];
+  d.k1hi = d.k1lo_all[R + 1];
+  d.k1max = 1;
+  for (int q = 0; q < W; ++q) d.k1max = std::max<int64_t>(d.k1max, d.k1lo_all[q + 1] - d.k1lo_all[q]);
+  std::vector<int32_t> si(sr.begin(), sr.begin() + std::max<int64_t>(nsend, 1)), ri(rr.begin(), rr.begin() + std::max<int64_t>(nrecv, 1));
+  d.send_idx.alloc(si.size()); d.recv_idx.alloc(ri.size());
+  MSP_CUDA(cudaMemcpy(d.send_idx.p, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
+  MSP_CUDA(cudaMemcpy(d.recv_idx.p, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice));
+  d.sendbuf.alloc(std::max<int64_t>(nsend, 1)); d.recvbuf.alloc(std::max<int64_t>(nrecv, 1));
+  d.gbuf_send.alloc(d.k1max); d.gbuf_recv.alloc(d.k1max * W);
+
+  const int64_t n = h.n;
+  const Lv lv = make_level_table(h);
+  cudaEvent_t e0, e1;
+  MSP_CUDA(cudaEventCreate(&e0));
+  MSP_CUDA(cudaEventCreate(&e1));
+  const int64_t launches0 = h.launches;
+  MSP_CUDA(cudaEventRecord(e0, st));
+  MSP_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+  MSP_CUDA(cudaMemcpyAsync(h.vr.p, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  MSP_CUDA(cudaMemsetAsync(h.vp.p, 0, n * sizeof(double), st));
+  launch(k_init_state, 1u, 1u, 0, st, h.scal.p, h.counters.p, rtol * rtol);
+  Prof P(h, st);
+  msp_sweeps(h, lv, nullptr, h.vr.p, h.vz.p, st, M_INIT, P, &d);
+  const unsigned gr = std::min<unsigned>(grid_for(std::max<int64_t>(d.row1 - d.row0, 1)), 148u * 4u);
+  int it = 0;
+  bool done = read_done(h, st);
+  while (!done && it < maxit) {
+    // p = z + beta p (own rows), halo exchange of p, q = L p, (p, q)
+    k_dist_p<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vz.p, h.vp.p, x, h.scal.p, h.counters.p);
+    if (nsend) k_take<<<grid_for(nsend), TPB, 0, st>>>(nsend, d.send_idx.p, h.vp.p, d.sendbuf.p);
+    MSP_LAUNCH_CHECK();
+    comm_check(d.comm.alltoallv(d.sendbuf.p, d.send_counts.data(), d.recvbuf.p, d.recv_counts.data(), d.comm.ctx),
+               "alltoallv(p halo)");
+    if (nrecv) k_put<<<grid_for(nrecv), TPB, 0, st>>>(nrecv, d.recv_idx.p, d.recvbuf.p, h.vp.p);
+    launch(k_spmv<false>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
+           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
+           (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
+           (const double*)h.w1.p, (const double*)h.vp.p, (const double*)nullptr, (double*)nullptr, h.vq.p,
+           (double*)nullptr, h.red.p, h.scal.p, h.counters.p, d.row0, d.row1);
+    k_dot_rows<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vp.p, h.vq.p, h.red.p, h.scal.p, h.counters.p, (int)S_PQ);
+    MSP_LAUNCH_CHECK();
+    comm_check(d.comm.allreduce(h.scal.p + S_PQ, 1, d.comm.ctx), "allreduce(pq)");
+    k_dist_finish<<<1, 1, 0, st>>>(0, h.scal.p, h.counters.p, M_ITER);
+    h.launches += 6;
+    // r -= alpha q, (r, r), z = R r, (r, z)
+    msp_sweeps(h, lv, h.vq.p, h.vr.p, h.vz.p, st, M_ITER, P, &d);
+    ++it;
+    done = read_done(h, st);
+  }
+  // x += alpha p for the last direction (own rows)
+  {
+    unsigned c[C_NCNT];
+    MSP_CUDA(cudaMemcpyAsync(c, h.counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    MSP_CUDA(cudaStreamSynchronize(st));
+    if (c[C_IT] > 0) {
+      MSP_CUDA(cudaMemsetAsync(h.counters.p + C_DONE, 0, sizeof(unsigned), st));
+      k_dist_p<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vz.p, h.vp.p, x, h.scal.p, h.counters.p);
+      MSP_LAUNCH_CHECK();
+      if (c[C_DONE]) MSP_CUDA(cudaMemcpyAsync(h.counters.p + C_DONE, &c[C_DONE], sizeof(unsigned), cudaMemcpyHostToDevice, st));
+    }
+  }
+  MSP_CUDA(cudaEventRecord(e1, st));
+  MSP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  MSP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  double hs[S_NSCAL];
+  unsigned hc[C_NCNT];
+  MSP_CUDA(cudaMemcpy(hs, h.scal.p, sizeof(hs), cudaMemcpyDeviceToHost));
+  MSP_CUDA(cudaMemcpy(hc, h.counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
+  if (rep) {
+    rep->iterations = (int32_t)hc[C_IT];
+    rep->converged = hc[C_DONE] ? 1 : 0;
+    rep->relres = hs[S_BB] > 0 ? std::sqrt(hs[S_RR] / hs[S_BB]) : 0.0;
+    rep->solve_ms = ms;
+    rep->kernel_launches = h.launches - launches0;
+  }
+  h.dist_row0 = d.row0;
+  h.dist_row1 = d.row1;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+__global__ void k_zero_outside(int64_t n, int64_t r0, int64_t r1, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && (i < r0 || i >= r1)) x[i] = 0.0;
+}
+
+void zero_outside(Handle& h, double* x, cudaStream_t st) {
+  k_zero_outside<<<grid_for(h.n), TPB, 0, st>>>(h.n, h.dist_row0, h.dist_row1, x);
+  MSP_LAUNCH_CHECK();
+}
+
+}  // namespace msp
+

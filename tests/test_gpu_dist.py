@@ -1,0 +1,88 @@
+"""The partitioned (multi-GPU) solve path on one GPU: world size 1 over NCCL
+(the only multi-rank configuration a single GPU may run; world >= 2 host
+logic is covered by tests/test_dist_plan.py with gloo).  The partitioned
+driver -- own-rows SpMV with the halo exchange, all-reduced dots, all-gathered
+y at the first tier's top level, replicated coarse levels -- against the
+oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from inputs import graphs as G
+from oracle import aggregation as A
+from oracle import expansion as E
+from oracle import graph as GR
+from oracle import pcg as PC
+from oracle import precond as PR
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+import paper_2207_07847_b200 as M  # noqa: E402
+from paper_2207_07847_b200.dist import TorchComm, dist_solve  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    yield TorchComm()
+    dist.destroy_process_group()
+
+
+def dt(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=DEV)
+
+
+@pytest.mark.parametrize("name,make", [("grid_90x70", lambda: G.grid2d(90, 70, "loguniform", 8)),
+                                       ("rgg_12000", lambda: G.rgg(12000, 12.0, 2))])
+def test_dist_solve_world1_matches_oracle(pg, name, make):
+    g = make()
+    S = M.setup(g.n, dt(g.rowptr, torch.int64), dt(g.col, torch.int32), dt(g.val), mu=0.8, seed=3)
+    b = G.rhs(g.n, 6)
+    out = dist_solve(S, pg, dt(b), rtol=1e-8, maxit=20000)
+    h = A.build_hierarchy(g, 3)
+    sysm = E.expand_msp_only(g, h, 0.8)
+    L = GR.laplacian_of_graph(g)
+    ref = PC.pcg(lambda v: L @ v, b, PR.msp(sysm), 1e-8, 20000)
+    single = S.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    assert out["converged"] == 1 and ref.converged
+    assert abs(out["iterations"] - single["iterations"]) <= 2, (out["iterations"], single["iterations"])
+    from test_gpu_parity import iteration_band
+    d = abs(out["iterations"] - ref.iterations)
+    if d > 2:
+        assert d <= iteration_band(L, b, sysm, ref.iterations), (name, out["iterations"], ref.iterations)
+    x = out["x"].cpu().numpy()
+    e = x - ref.x
+    e -= e.mean()
+    xs = ref.x - ref.x.mean()
+    assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs)), name
+
+
+def test_dist_solve_host_buffers_and_small_graph_error(pg):
+    g = G.grid2d(90, 70, "uniform1_10", 1)
+    S = M.setup(g.n, g.rowptr, g.col, g.val, mu=0.8)
+    b = G.rhs(g.n, 2)
+    out = dist_solve(S, pg, b.copy(), rtol=1e-8)
+    assert out["converged"] == 1
+    L = GR.laplacian_of_graph(g)
+    assert np.linalg.norm(L @ out["x"] - b) <= 1.01e-8 * np.linalg.norm(b)
+    tiny = G.grid2d(6, 6)
+    St = M.setup(tiny.n, tiny.rowptr, tiny.col, tiny.val)
+    with pytest.raises(M.MspError) as ei:
+        dist_solve(St, pg, G.rhs(tiny.n, 0))
+    assert ei.value.code == -4
