@@ -114,6 +114,7 @@ struct Handle {
   // padded with (self, 0)); rows of degree > LCAP are "long": empty in SELL,
   // flagged in sell_mask and handled warp-per-row from the nested CSR
   int64_t nslices = 0, nlong = 0;
+  int sell_maxw = 0;          // widest slice (padded row length)
   DBuf<int64_t> sell_ptr;
   DBuf<int32_t> sell_col;
   DBuf<double> sell_w;
@@ -161,6 +162,7 @@ struct Handle {
   DBuf<double> red;           // reduction partials
   DBuf<double> vx, vr, vp, vq, vz, vb;  // PCG vectors (nested numbering)
   DBuf<double> vp2;           // ping-pong partner of vp (p = z + beta p fused into L p)
+  DBuf<double> zp1, zp2;      // MSP path: interleaved (z_i, p_i) pairs, ping-pong
   int pparity = 0;            // which of vp / vp2 holds the current p
   cudaGraphExec_t graph = nullptr;  // captured batch of PCG iterations
   int graph_batch = 0;

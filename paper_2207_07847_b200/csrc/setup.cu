@@ -351,7 +351,8 @@ __global__ void k_hvec(int64_t nB, const int32_t* __restrict__ cptr, const doubl
 
 // ------------------------------------------------------------ SELL-32
 __global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restrict__ rowptr, int lcap,
-                             int64_t* __restrict__ width, uint32_t* __restrict__ mask, int32_t* __restrict__ islong) {
+                             int64_t* __restrict__ width, uint32_t* __restrict__ mask, int32_t* __restrict__ islong,
+                             int* __restrict__ maxw) {
   const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;  // warp-uniform
@@ -364,7 +365,7 @@ __global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restri
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
   const uint32_t m = __ballot_sync(0xffffffffu, lng);
-  if (lane == 0) { width[s] = 32 * (int64_t)w; mask[s] = m; }
+  if (lane == 0) { width[s] = 32 * (int64_t)w; mask[s] = m; atomicMax(maxw, w); }
 }
 
 __global__ void k_sell_fill(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
@@ -808,7 +809,12 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     h.sell_mask.alloc(ns);
     h.sell_ptr.alloc(ns + 1);
     MSP_CUDA(cudaMemsetAsync(width.p + ns, 0, sizeof(int64_t), st));
-    k_sell_width<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.rowptr1.p, lcap, width.p, h.sell_mask.p, islong.p);
+    DBuf<int> mw;
+    mw.alloc(1);
+    MSP_CUDA(cudaMemsetAsync(mw.p, 0, sizeof(int), st));
+    k_sell_width<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.rowptr1.p, lcap, width.p, h.sell_mask.p, islong.p,
+                                                    mw.p);
+    h.sell_maxw = d2h_scalar(mw.p, st);
     MSP_LAUNCH_CHECK();
     exclusive_scan(tmp, width.p, h.sell_ptr.p, ns + 1, st);
     const int64_t tot = d2h_scalar(h.sell_ptr.p + ns, st);

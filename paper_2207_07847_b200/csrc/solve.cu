@@ -54,6 +54,9 @@ enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
 enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2, M_COLUMN = 3 };
 // multi-GPU: local totals only (the caller all-reduces, k_dist_finish derives)
 constexpr int M_DIST = 16;
+// level-1 output z interleaved with p ([z_i, p_i] pairs, index 2i): the
+// fused SpMV then gathers one 16-byte pair per neighbour
+constexpr int M_ZS2 = 32;
 
 // phase timestamps for kernel-structure work (build with -DMSP_TRACE; the
 // in-tree library never defines it)
@@ -360,6 +363,116 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
   }
 }
 
+
+// Software-pipelined SELL SpMV for slices no wider than MW (fused PCG form):
+// while slice s is gathered and reduced, the slice pointers of s+2 and the
+// column / weight / row vectors of s+1 are already in flight.
+template <int MW>
+__global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
+                                                      const int32_t* __restrict__ scol, const double* __restrict__ sw,
+                                                      const uint32_t* __restrict__ smask, int64_t nlong,
+                                                      const int32_t* __restrict__ long_rows,
+                                                      const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                      const double* __restrict__ w, const double2* __restrict__ zp,
+                                                      double* __restrict__ zpout,
+                                                      double* __restrict__ q, double* __restrict__ x,
+                                                      double* __restrict__ part, double* __restrict__ scal,
+                                                      unsigned int* __restrict__ cnt) {
+  // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
+  pdl_wait();
+  if (cnt[C_DONE]) return;
+  const double beta = scal[S_BETA];
+  const double alpha = scal[S_ALPHA];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)TPB + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * TPB) >> 5;
+  double d = 0.0;
+  // stage A (slice s): pointers; stage B (slice s): columns, weights, own row
+  int64_t s = warp;
+  int64_t b0 = 0, b1 = 0;
+  if (s < nslices) { b0 = sptr[s]; b1 = sptr[s + 1]; }
+  int32_t jc[MW];
+  double wc[MW];
+  double po = 0.0, zr = 0.0;
+  uint32_t mk = 0;
+  auto load_B = [&](int64_t ss, int64_t bb0, int64_t bb1) {
+    const int wd = (int)((bb1 - bb0) >> 5);
+    const int64_t r = ss * 32 + lane;
+#pragma unroll
+    for (int k = 0; k < MW; ++k) {
+      if (k < wd) {
+        jc[k] = scol[bb0 + k * 32 + lane];
+        wc[k] = sw[bb0 + k * 32 + lane];
+      }
+    }
+    mk = smask[ss];
+    if (r < n) { const double2 v = zp[r]; zr = v.x; po = v.y; }
+  };
+  if (s < nslices) load_B(s, b0, b1);
+  while (s < nslices) {
+    const int64_t s1 = s + nwarps;
+    int64_t n0 = 0, n1 = 0;
+    if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
+    // current slice: gathers and reduction
+    const int wd = (int)((b1 - b0) >> 5);
+    const int64_t r = s * 32 + lane;
+    const double pi = zr + beta * po;
+    double g[MW];
+#pragma unroll
+    for (int k = 0; k < MW; ++k)
+      if (k < wd) {
+        const double2 v = zp[jc[k]];
+        g[k] = v.x + beta * v.y;
+      }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MW; ++k)
+      if (k < wd) acc += wc[k] * (pi - g[k]);
+    if (r < n && !((mk >> lane) & 1u)) {
+      q[r] = acc;
+      zpout[2 * r + 1] = pi;
+      x[r] += alpha * po;
+      d += pi * acc;
+    }
+    // next slice's columns / weights / row vectors
+    s = s1;
+    b0 = n0;
+    b1 = n1;
+    if (s < nslices) load_B(s, b0, b1);
+  }
+  for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
+    const int64_t r = long_rows[i];
+    const double2 vr = zp[r];
+    const double pr = vr.y;
+    const double pi = vr.x + beta * pr;
+    double acc = 0.0;
+    for (int32_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+      const double2 v = zp[col[e]];
+      acc += w[e] * (pi - (v.x + beta * v.y));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      q[r] = acc;
+      zpout[2 * r + 1] = pi;
+      x[r] += alpha * pr;
+      d += pi * acc;
+    }
+  }
+  pdl_trigger();
+  const double bs = block_sum<TPB>(d);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) part[blockIdx.x] = bs;
+    if (warp_last_block(&cnt[C_SPMV])) {
+      const double pq = warp_sum_partials(part, gridDim.x);
+      if (threadIdx.x == 0) {
+        scal[S_PQ] = pq;
+        scal[S_ALPHA] = scal[S_RHO] / pq;
+        cnt[C_SPMV] = 0;
+      }
+    }
+  }
+}
+
 // x += alpha p for the last direction (the in-loop updates are deferred into
 // the next L p); p is the buffer the C_IT-th product wrote
 __global__ void k_x_final(int64_t n, double* __restrict__ x, const double* __restrict__ vp,
@@ -404,6 +517,20 @@ __device__ __forceinline__ int stage_window(uint64_t* bar, char* dst, const void
     tma_1d(dst, (const char*)src + a0 * es, bytes, bar);
   }
   return (int)(lo - a0);
+}
+
+// same for the interleaved (z, p) pairs: iteration k writes p into the
+// buffer of parity k & 1
+__global__ void k_x_final_pairs(int64_t n, double* __restrict__ x, const double* __restrict__ zp1,
+                                const double* __restrict__ zp2, const double* __restrict__ scal,
+                                const unsigned* __restrict__ cnt) {
+  pdl_wait();
+  const unsigned it = cnt[C_IT];
+  if (it == 0) return;
+  const double* zp = (it & 1u) ? zp2 : zp1;
+  const double alpha = scal[S_ALPHA];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += alpha * zp[2 * i + 1];
 }
 
 // ------------------------------------------------------------ tile up-sweep
@@ -715,7 +842,8 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     const double* nc = SMP(const double, tb[0].nn >= 0 ? tb[0].nn : 0);
     const int ac = tb[0].a, npar = tb[1].cnt;
     const double ckk = tb[0].ck;
-    double* zg = FIRST ? zout + ac : Zg + lv.off[k0 - 1] + ac;
+    const int zs = (mode_in & M_ZS2) ? 2 : 1;
+    double* zg = FIRST ? zout + zs * ac : Zg + lv.off[k0 - 1] + ac;
     double* wg = Wg + lv.off[k0 - 1] + ac;
     for (int i = tid; i < npar; i += TT) {
       const int lb = -3 * (2 * i + 2);
@@ -724,7 +852,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
             cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
             [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
             [&](int p) { return yc[p] - rho; },
-            [&](int p, double z, double w) { rz += yc[p] * w; zg[p] = w; });
+            [&](int p, double z, double w) { rz += yc[p] * w; zg[zs * p] = w; });
       else
         block_solve(
             cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
@@ -758,7 +886,8 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
 // aggregate)  y_{k+1} = P^T y_k
 __global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
                                                 const double* __restrict__ yin, double* __restrict__ yout,
-                                                const unsigned int* __restrict__ cnt, int mode) {
+                                                const unsigned int* __restrict__ cnt, int mode_in) {
+  const int mode = mode_in & 15;
   pdl_wait();
   if (mode == M_ITER && cnt[C_DONE]) return;
   const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -778,7 +907,9 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
                                                   const double* __restrict__ zB, const double* __restrict__ wB,
                                                   double* __restrict__ zk, double* __restrict__ wk,
                                                   double* __restrict__ part, double* __restrict__ scal,
-                                                  unsigned int* __restrict__ cnt, int mode) {
+                                                  unsigned int* __restrict__ cnt, int mode_in) {
+  const int mode = mode_in & 15;
+  const int zs = (mode_in & M_ZS2) ? 2 : 1;
   pdl_wait();
   if (mode != M_APPLY && cnt[C_DONE]) return;
   const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -794,7 +925,7 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
         cp[B], cp[B + 1], [&](int j) { return ki[j]; }, [&](int64_t p, int j) { return lof[lb + 3 * p + j]; }, zB[B],
         lv.negmu * wB[B], [&](int64_t p) { return LEVEL1 ? yk[p] - rho : ckk * yk[p] - rho * Nk[p]; },
         [&](int64_t p, double z, double w) {
-          if (LEVEL1) { rz += yk[p] * w; wk[p] = w; }
+          if (LEVEL1) { rz += yk[p] * w; wk[zs * p] = w; }
           else { zk[p] = z; wk[p] = w; }
         });
   }
@@ -949,7 +1080,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     const double z = zt[i] - m;
     zt[i] = z;
     wt[i] = z;
-    if (L == 1) { rz += yt[i] * z; zout[i] = z; }
+    if (L == 1) { rz += yt[i] * z; zout[((mode_in & M_ZS2) ? 2 : 1) * i] = z; }
   }
   TRACE(5);
   // ---- down
@@ -974,7 +1105,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
           cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
           zp[i], negmu * wp[i], [&](int p) { return out1 ? yc[p] - rho : ckk * yc[p] - rho * nc[p]; },
           [&](int p, double z, double w) {
-            if (out1) { rz += yc[p] * w; zout[p] = w; }
+            if (out1) { rz += yc[p] * w; zout[((mode_in & M_ZS2) ? 2 : 1) * p] = w; }
             else { zc[p] = z; wc[p] = w; }
           });
     }
@@ -1229,6 +1360,7 @@ void dist_after_tier1_down(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
 
 void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P,
                 DistCtx* dc = nullptr) {
+  const int mbase = mode & 15;
   double* part_rr = h.red.p;                  // [cap/4]
   double* part_rz = h.red.p + h.red_cap / 4;
   double* part_gd = h.red.p + h.red_cap / 2;
@@ -1257,7 +1389,7 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
     }
     ++h.launches;
-    if (dc && i == 0 && !dist_after_tier1_up(h, *dc, st, mode)) return;  // converged
+    if (dc && i == 0 && !dist_after_tier1_up(h, *dc, st, mbase)) return;  // converged
   }
   // ---- coarse (folded into the top tier's down kernel in GEMV mode)
   if (!h.gemv) {
@@ -1307,7 +1439,7 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     }
     ++h.launches;
   }
-  if (dc) dist_after_tier1_down(h, *dc, st, mode);
+  if (dc) dist_after_tier1_down(h, *dc, st, mbase);
 }
 
 template <bool PCG>
@@ -1320,9 +1452,38 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
   ++h.launches;
 }
 
+// SpMV of the MSP iteration on interleaved (z, p) pairs (M_ZS2)
+void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
+  auto go = [&](auto kern) {
+    launch(kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
+           (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, (const int32_t*)h.long_rows.p,
+           (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
+           reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
+  };
+  if (h.sell_maxw <= 4) go(k_spmv_pipe<4>);
+  else if (h.sell_maxw <= 8) go(k_spmv_pipe<8>);
+  else go(k_spmv_pipe<16>);
+  ++h.launches;
+}
+
+bool use_pairs(const Handle& h) {
+  static const bool off = std::getenv("MSP_NO_SPMV_PIPE") != nullptr;
+  return !off && h.sell_maxw <= 16;
+}
+
 // one PCG iteration (reading R10): p = z + beta p, q = L p (x += alpha p
 // deferred), r -= alpha q, z = R r
 void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t st, Prof& P) {
+  if (precond == MSP_PRECOND_MSP && use_pairs(h)) {
+    double* zin = h.pparity ? h.zp2.p : h.zp1.p;
+    double* zout = h.pparity ? h.zp1.p : h.zp2.p;
+    h.pparity ^= 1;
+    P.begin();
+    launch_spmv_pairs(h, zin, zout, h.vq.p, x, st);
+    P.end(PC_SPMV);
+    msp_sweeps(h, lv, h.vq.p, h.vr.p, zout, st, M_ITER | M_ZS2, P);
+    return;
+  }
   double* pold = h.pparity ? h.vp2.p : h.vp.p;
   double* pnew = h.pparity ? h.vp.p : h.vp2.p;
   h.pparity ^= 1;
@@ -1390,6 +1551,7 @@ void alloc_solve_workspace(Handle& h) {
     MSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     int per_sm = 8;
     if (const char* e = std::getenv("MSP_SPMV_BLOCKS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+    else per_sm = 4;
     const int64_t want = grid_for(std::max<int64_t>(h.nslices, 1) * 32);
     h.spmv_grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * per_sm);
   }
@@ -1403,6 +1565,10 @@ void alloc_solve_workspace(Handle& h) {
   for (auto* v : {&h.vx, &h.vr, &h.vp, &h.vp2, &h.vq, &h.vz, &h.vb}) {
     v->alloc(h.n + 8);
     MSP_CUDA(cudaMemset(v->p, 0, (h.n + 8) * sizeof(double)));
+  }
+  for (auto* v : {&h.zp1, &h.zp2}) {
+    v->alloc(2 * h.n + 8);
+    MSP_CUDA(cudaMemset(v->p, 0, (2 * h.n + 8) * sizeof(double)));
   }
   h.counters.alloc(C_NCNT);
   h.scal.alloc(S_NSCAL);
@@ -1460,7 +1626,10 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
   ++h.launches;
   {
     Prof P(h, st);
-    if (precond == MSP_PRECOND_MSP) {
+    if (precond == MSP_PRECOND_MSP && use_pairs(h)) {
+      MSP_CUDA(cudaMemsetAsync(h.zp1.p, 0, 2 * n * sizeof(double), st));
+      msp_sweeps(h, lv, nullptr, h.vr.p, h.zp1.p, st, M_INIT | M_ZS2, P);
+    } else if (precond == MSP_PRECOND_MSP) {
       msp_sweeps(h, lv, nullptr, h.vr.p, h.vz.p, st, M_INIT, P);
     } else if (precond == MSP_PRECOND_NONE) {
       launch(k_update_cg, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, h.vr.p, (const double*)nullptr,
@@ -1546,8 +1715,12 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
     if (host_cnt[C_DONE]) break;
   }
   }
-  launch(k_x_final, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, x, (const double*)h.vp.p,
-         (const double*)h.vp2.p, (const double*)h.scal.p, (const unsigned*)h.counters.p);
+  if (precond == MSP_PRECOND_MSP && use_pairs(h))
+    launch(k_x_final_pairs, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, x, (const double*)h.zp1.p,
+           (const double*)h.zp2.p, (const double*)h.scal.p, (const unsigned*)h.counters.p);
+  else
+    launch(k_x_final, std::min<unsigned>(grid_for(n), 148u * 8u), TPB, 0, st, n, x, (const double*)h.vp.p,
+           (const double*)h.vp2.p, (const double*)h.scal.p, (const unsigned*)h.counters.p);
   ++h.launches;
   MSP_CUDA(cudaEventRecord(e1, st));
   MSP_CUDA(cudaEventSynchronize(e1));
