@@ -115,6 +115,7 @@ struct Handle {
   // flagged in sell_mask and handled warp-per-row from the nested CSR
   int64_t nslices = 0, nlong = 0;
   int sell_maxw = 0;          // widest slice (padded row length)
+  bool sell_uniform = false;  // every slice padded to sell_maxw (no slice pointers needed)
   DBuf<int64_t> sell_ptr;
   DBuf<int32_t> sell_col;
   DBuf<double> sell_w;

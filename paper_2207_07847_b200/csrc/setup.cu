@@ -350,6 +350,11 @@ __global__ void k_hvec(int64_t nB, const int32_t* __restrict__ cptr, const doubl
 }
 
 // ------------------------------------------------------------ SELL-32
+__global__ void k_fill_uniform_ptr(int64_t ns, int64_t stride, int64_t* __restrict__ sptr) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s <= ns) sptr[s] = s * stride;
+}
+
 __global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restrict__ rowptr, int lcap,
                              int64_t* __restrict__ width, uint32_t* __restrict__ mask, int32_t* __restrict__ islong,
                              int* __restrict__ maxw) {
@@ -817,7 +822,16 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     h.sell_maxw = d2h_scalar(mw.p, st);
     MSP_LAUNCH_CHECK();
     exclusive_scan(tmp, width.p, h.sell_ptr.p, ns + 1, st);
-    const int64_t tot = d2h_scalar(h.sell_ptr.p + ns, st);
+    int64_t tot = d2h_scalar(h.sell_ptr.p + ns, st);
+    // uniform slices (every slice padded to the widest) when that costs
+    // < 10% padding: the SpMV then needs no slice pointers at all
+    h.sell_uniform = std::getenv("MSP_SELL_NONUNIFORM") == nullptr && h.sell_maxw > 0 &&
+                     (double)ns * 32 * h.sell_maxw <= 1.1 * (double)tot;
+    if (h.sell_uniform) {
+      k_fill_uniform_ptr<<<grid_for(ns + 1), TPB, 0, st>>>(ns, 32 * (int64_t)h.sell_maxw, h.sell_ptr.p);
+      MSP_LAUNCH_CHECK();
+      tot = ns * 32 * (int64_t)h.sell_maxw;
+    }
     h.sell_col.alloc(std::max<int64_t>(tot, 1));
     h.sell_w.alloc(std::max<int64_t>(tot, 1));
     k_sell_fill<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.sell_ptr.p, h.rowptr1.p, h.col1.p, h.w1.p,

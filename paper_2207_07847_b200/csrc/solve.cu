@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 // Software-pipelined SELL SpMV for slices no wider than MW (fused PCG form):
 // while slice s is gathered and reduced, the slice pointers of s+2 and the
 // column / weight / row vectors of s+1 are already in flight.
-template <int MW>
+template <int MW, bool UNIF>
 __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
                                                       const uint32_t* __restrict__ smask, int64_t nlong,
@@ -390,13 +390,14 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
   // stage A (slice s): pointers; stage B (slice s): columns, weights, own row
   int64_t s = warp;
   int64_t b0 = 0, b1 = 0;
-  if (s < nslices) { b0 = sptr[s]; b1 = sptr[s + 1]; }
+  if (UNIF) { b0 = s * 32 * MW; b1 = b0 + 32 * MW; }
+  else if (s < nslices) { b0 = sptr[s]; b1 = sptr[s + 1]; }
   int32_t jc[MW];
   double wc[MW];
   double po = 0.0, zr = 0.0;
   uint32_t mk = 0;
   auto load_B = [&](int64_t ss, int64_t bb0, int64_t bb1) {
-    const int wd = (int)((bb1 - bb0) >> 5);
+    const int wd = UNIF ? MW : (int)((bb1 - bb0) >> 5);
     const int64_t r = ss * 32 + lane;
 #pragma unroll
     for (int k = 0; k < MW; ++k) {
@@ -412,9 +413,10 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
   while (s < nslices) {
     const int64_t s1 = s + nwarps;
     int64_t n0 = 0, n1 = 0;
-    if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
+    if (UNIF) { n0 = s1 * 32 * MW; n1 = n0 + 32 * MW; }
+    else if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
     // current slice: gathers and reduction
-    const int wd = (int)((b1 - b0) >> 5);
+    const int wd = UNIF ? MW : (int)((b1 - b0) >> 5);
     const int64_t r = s * 32 + lane;
     const double pi = zr + beta * po;
     double g[MW];
@@ -1460,9 +1462,12 @@ void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
   };
-  if (h.sell_maxw <= 4) go(k_spmv_pipe<4>);
-  else if (h.sell_maxw <= 8) go(k_spmv_pipe<8>);
-  else go(k_spmv_pipe<16>);
+  if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
+  else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true>);
+  else if (h.sell_uniform && h.sell_maxw == 8) go(k_spmv_pipe<8, true>);
+  else if (h.sell_maxw <= 4) go(k_spmv_pipe<4, false>);
+  else if (h.sell_maxw <= 8) go(k_spmv_pipe<8, false>);
+  else go(k_spmv_pipe<16, false>);
   ++h.launches;
 }
 
