@@ -107,26 +107,31 @@ class ClockSampler:
 # kernel must touch, once; gathered neighbour values are L2 re-reads and are
 # not counted.
 def spmv_bytes(n: int, nnz_adj: int) -> int:
-    """p = z + beta p_old fused with q = L_G p and (p, q): per row the int32
-    row offset, z_i and p_old_i read, p_i and q_i written (4 + 4*8 B); per
-    adjacency entry an int32 column and an fp64 weight (12 B)."""
-    return n * 36 + nnz_adj * 12
+    """p = z + beta p_old fused with q = L_G p, (p, q) and the deferred
+    x += alpha p_old: per row the (z_i, p_old_i) pair read, p_i and q_i
+    written, x_i read and written (48 B); per adjacency entry an int32 column
+    and an fp64 weight (12 B).  SELL padding and gathered neighbour pairs
+    (L2 re-reads) are not counted."""
+    return n * 48 + nnz_adj * 12
 
 
 def tile_up_bytes(sizes, kt: int) -> int:
-    """x += a p, r -= a q (x, p, r, q read, x, r written: 48 B per level-1
-    node); g read for levels 1..Kt (8 B); child pointers of levels 2..Kt
-    (4 B); y written at level Kt (8 B)."""
+    """r -= a q, (r, r), (r, H): r, q, H read and r written (32 B per
+    level-1 node); descendant offsets of the level-Kt nodes (4 B) and y
+    written at level Kt (8 B)."""
     n = sizes[0]
-    return 48 * n + 8 * sum(sizes[:kt]) + 4 * sum(sizes[1:kt]) + 8 * sizes[kt - 1] * (kt > 1)
+    return 32 * n + 12 * sizes[kt - 1]
 
 
 def tile_down_bytes(sizes, kt: int) -> int:
-    """r read and R r written (16 B per level-1 node); factors c0, c1, c2 of
-    levels 1..Kt-1 (24 B); subtree sizes N of levels 2..Kt-1 (8 B); child
-    pointers of levels 2..Kt (4 B); z, w read at level Kt (16 B)."""
+    """r read and R r written (16 B per level-1 node); the packed factors:
+    K'^{-1} of every aggregate at levels 2..Kt (24 B each) and the
+    coefficients of the leftovers among levels 1..Kt-1 (24 B each, n_k -
+    2 n_{k+1} of them); child pointers of levels 2..Kt (4 B); z, w read at
+    level Kt (16 B).  Subtree sizes are recomputed in shared memory."""
     n = sizes[0]
-    return (16 * n + 24 * sum(sizes[:kt - 1]) + 8 * sum(sizes[1:kt - 1]) + 4 * sum(sizes[1:kt])
+    leftovers = sum(sizes[k] - 2 * sizes[k + 1] for k in range(kt - 1))
+    return (16 * n + 24 * sum(sizes[1:kt]) + 24 * leftovers + 4 * sum(sizes[1:kt])
             + 16 * sizes[kt - 1])
 
 
