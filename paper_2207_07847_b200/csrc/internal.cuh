@@ -132,6 +132,7 @@ struct Handle {
     bool generic = false;     // one level by per-node kernels (an aggregate too large to tile)
     TierDesc desc{};
     DBuf<int32_t> firstk0;    // [n_k1 + 1]: first level-k0 descendant of each level-k1 node
+    int up_group = 1;         // tiles per CTA of the up kernel
   };
   std::vector<Tier> tiers;
   int32_t Kc = 1;

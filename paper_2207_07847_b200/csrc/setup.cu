@@ -1025,6 +1025,8 @@ void build_schedule(Handle& h, cudaStream_t st) {
       t.desc.k0 = 1;
       t.desc.nl = 1;
       t.desc.ntiles = (int)t.ntiles;
+      t.desc.up_group = 1;
+      t.up_group = 1;
     } else {
       k_tile_bounds<<<grid_for(nt1), TPB, 0, st>>>(t.ntiles, h.lv[k1_ - 1].n, T, first_k1->p,
                                                     t.tstart.p + (int64_t)(nl - 1) * nt1);
@@ -1051,6 +1053,23 @@ void build_schedule(Handle& h, cudaStream_t st) {
       }
       const bool top = (k1_ == h.Kc) && gemv_ok;
       t.desc = tier_layout(k0_, nl, t.ntiles, cap, caplo, top ? h.lv[h.Kc - 1].n : 0);
+      // the up kernel takes `up_group` consecutive tiles per CTA (its level-1
+      // pass is a plain stream; more work per CTA amortises the fixed cost)
+      {
+        int G = (k0_ == 1) ? 4 : 1;
+        if (const char* e = std::getenv("MSP_UP_GROUP")) G = (k0_ == 1) ? std::max(1, std::atoi(e)) : 1;
+        int64_t c0 = 0, c1 = 0;
+        for (int64_t j = 0; j < t.ntiles; j += G) {
+          const int64_t je = std::min<int64_t>(j + G, t.ntiles);
+          c0 = std::max<int64_t>(c0, ts[je] - ts[j]);
+          c1 = std::max<int64_t>(c1, ts[(size_t)(nl - 1) * nt1 + je] - ts[(size_t)(nl - 1) * nt1 + j]);
+        }
+        t.up_group = G;
+        t.desc.o_uf = 0;
+        t.desc.o_uy0 = a16((c1 + 1 + 8) * 4);
+        t.desc.smem_up = a16(t.desc.o_uy0 + (c0 + 2) * 8);
+        t.desc.up_group = G;
+      }
       const int64_t nk1 = h.lv[k1_ - 1].n;
       t.firstk0.alloc(nk1 + 1 + 8);
       MSP_CUDA(cudaMemsetAsync(t.firstk0.p, 0, (nk1 + 1 + 8) * sizeof(int32_t), st));

@@ -554,15 +554,19 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone;
-  const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  // this CTA's tiles [tA, tB): `group` consecutive tiles (1 when distributed)
+  const int grp = (mode_in & M_DIST) ? 1 : td.up_group;
+  const int tA = tile0 + blockIdx.x * grp, tB = min(tA + grp, td.ntiles);
+  const int tile = (mode_in & M_DIST) ? tA : blockIdx.x;  // partial-sum slot
+  const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&bar, 1);
-    sa0 = tstart[tile];
-    sn0 = tstart[tile + 1] - sa0;
+    sa0 = tstart[tA];
+    sn0 = tstart[tB] - sa0;
     if (nl > 1) {
-      sa1 = tstart[(nl - 1) * nt1 + tile];
-      sn1 = tstart[(nl - 1) * nt1 + tile + 1] - sa1;
+      sa1 = tstart[(nl - 1) * nt1 + tA];
+      sn1 = tstart[(nl - 1) * nt1 + tB] - sa1;
       skf = stage_window(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
     }
   }
@@ -1381,11 +1385,12 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(PC_MID_UP);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : T.ntiles), TT, T.smem_up, st, lv,
+        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), TT,
+               T.smem_up, st, lv,
                T.desc, (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p,
                h.Y.p, part_rr, part_gd, scal, cnt, mode | (dc ? M_DIST : 0), (int)(dc ? dc->tile0 : 0));
       else
-        launch(k_tile_up<false>, (unsigned)T.ntiles, TT, T.smem_up, st, lv, T.desc,
+        launch(k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), TT, T.smem_up, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
                part_rr, part_gd, scal, cnt, mode, 0);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
@@ -1399,7 +1404,8 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
     launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
            (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
-           y0, h.Z.p, h.W.p, z, (const double*)part_gd, (int)h.tiers[0].ntiles, scal, cnt,
+           y0, h.Z.p, h.W.p, z, (const double*)part_gd,
+           (int)((h.tiers[0].ntiles + h.tiers[0].up_group - 1) / h.tiers[0].up_group), scal, cnt,
            mode | (dc ? M_DIST : 0));
     P.end(PC_COARSE);
     ++h.launches;
