@@ -44,7 +44,7 @@ struct TierDesc {
   int smem_down;
   // up kernel (its own layout): first level-k0 descendant of each level-k1
   // node of the tile (int32, [a, b]) and y at level k0
-  int o_uf, o_uy0, smem_up;
+  int o_uf, o_uy0, o_uq, o_uh, smem_up;
   int up_group;    // tiles per CTA of the up kernel (1 when distributed)
 };
 

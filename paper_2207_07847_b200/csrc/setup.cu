@@ -1021,7 +1021,13 @@ void build_schedule(Handle& h, cudaStream_t st) {
       k_tile_bounds<<<grid_for(nt1), TPB, 0, st>>>(t.ntiles, n0, T, id.p, t.tstart.p);
       MSP_LAUNCH_CHECK();
       MSP_CUDA(cudaStreamSynchronize(st));
-      t.smem_up = 0;  // level 1 only: nothing staged
+      // level 1 only: the r, q, H windows of one tile of T rows
+      t.desc.o_uf = 0;
+      t.desc.o_uy0 = 16;
+      t.desc.o_uq = a16(t.desc.o_uy0 + (T + 2) * 8);
+      t.desc.o_uh = a16(t.desc.o_uq + (T + 2) * 8);
+      t.desc.smem_up = a16(t.desc.o_uh + (T + 2) * 8);
+      t.smem_up = t.desc.smem_up;
       t.desc.k0 = 1;
       t.desc.nl = 1;
       t.desc.ntiles = (int)t.ntiles;
@@ -1066,8 +1072,10 @@ void build_schedule(Handle& h, cudaStream_t st) {
         }
         t.up_group = G;
         t.desc.o_uf = 0;
-        t.desc.o_uy0 = a16((c1 + 1 + 8) * 4);
-        t.desc.smem_up = a16(t.desc.o_uy0 + (c0 + 2) * 8);
+        t.desc.o_uy0 = a16((c1 + 1 + 8) * 4);            // r (FIRST: staged, updated in place) or y_k0
+        t.desc.o_uq = a16(t.desc.o_uy0 + (c0 + 2) * 8);  // q (FIRST)
+        t.desc.o_uh = a16(t.desc.o_uq + (c0 + 2) * 8);   // H (FIRST)
+        t.desc.smem_up = (k0_ == 1) ? a16(t.desc.o_uh + (c0 + 2) * 8) : a16(t.desc.o_uy0 + (c0 + 2) * 8);
         t.desc.up_group = G;
       }
       const int64_t nk1 = h.lv[k1_ - 1].n;

@@ -541,6 +541,8 @@ __global__ void k_x_final_pairs(int64_t n, double* __restrict__ x, const double*
 // staged from Y.  y_k1 = (P^T)^{k1-k0} y_k0 is formed directly, each level-k1
 // node summing its contiguous range of level-k0 descendants (one warp per
 // node), and written to global Y.
+#undef TRACE_KID
+#define TRACE_KID (FIRST ? 4 : 5)
 template <bool FIRST>
 __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
                                                 const int32_t* __restrict__ tstart, const int32_t* __restrict__ firstk0,
@@ -553,13 +555,15 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone;
+  __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone, skr, skq, skh;
+  __shared__ double salpha;
   // this CTA's tiles [tA, tB): `group` consecutive tiles (1 when distributed)
   const int grp = (mode_in & M_DIST) ? 1 : td.up_group;
   const int tA = tile0 + blockIdx.x * grp, tB = min(tA + grp, td.ntiles);
   const int tile = (mode_in & M_DIST) ? tA : blockIdx.x;  // partial-sum slot
   const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TRACE(0);
   if (tid == 0) {
     mbar_init(&bar, 1);
     sa0 = tstart[tA];
@@ -569,13 +573,27 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
       sn1 = tstart[(nl - 1) * nt1 + tB] - sa1;
       skf = stage_window(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
     }
+    // FIRST: the level-1 H (constant) and, in PCG iterations, r (last written
+    // by the previous iteration's up kernel) are staged before the grid
+    // dependency resolves; q after it
+    if (FIRST && sn0 > 0) {
+      skh = stage_window(&bar, sm + td.o_uh, H, 8, sa0, (int64_t)sa0 + sn0);
+      if (mode == M_ITER) skr = stage_window(&bar, sm + td.o_uy0, r, 8, sa0, (int64_t)sa0 + sn0);
+    }
   }
+  TRACE(1);
   pdl_wait();
+  TRACE(2);
   if (tid == 0) {
     sdone = (mode == M_ITER) ? (int)cnt[C_DONE] : 0;
+    salpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
     if (!FIRST && !sdone) {
       const int64_t base = lv.off[k0 - 1];
       sky0 = stage_window(&bar, sm + td.o_uy0, Yg, 8, base + sa0, base + sa0 + sn0);
+    }
+    if (FIRST && sn0 > 0) {
+      if (mode == M_ITER) skq = stage_window(&bar, sm + td.o_uq, q, 8, sa0, (int64_t)sa0 + sn0);
+      else skr = stage_window(&bar, sm + td.o_uy0, r, 8, sa0, (int64_t)sa0 + sn0);
     }
     mbar_arrive(&bar);
   }
@@ -583,43 +601,32 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   const int done = sdone;
   double rr = 0.0, gd = 0.0;
   double* y0 = reinterpret_cast<double*>(sm + td.o_uy0);
-  if (FIRST && !done) {  // level-1 update, overlapping the TMA of the descendant offsets
-    const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
-    const int a1 = sa0, n1 = sn0;
-    constexpr int U = 4;  // all loads of U elements issued before any use
-    for (int i0 = tid; i0 < n1; i0 += U * TT) {
-      double rv[U], qv[U], hv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * TT;
-        if (i < n1) {
-          rv[u] = r[a1 + i];
-          qv[u] = (mode == M_ITER) ? q[a1 + i] : 0.0;
-          hv[u] = H[a1 + i];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * TT;
-        if (i < n1) {
-          double ri = rv[u];
-          if (mode == M_ITER) {
-            ri -= alpha * qv[u];
-            r[a1 + i] = ri;
-          }
-          rr += ri * ri;
-          gd += hv[u] * ri;
-          if (nl > 1) y0[i] = ri;
-        }
-      }
-    }
-  }
+  TRACE(3);
   mbar_wait(&bar, 0);
+  TRACE(4);
   if (done) return;
+  if (FIRST) {  // level-1 update from shared memory; r_new in place of r (it is y_1)
+    const double alpha = salpha;
+    const int a1 = sa0, n1 = sn0;
+    double* rs = y0 + skr;
+    const double* qs = reinterpret_cast<const double*>(sm + td.o_uq) + skq;
+    const double* hs = reinterpret_cast<const double*>(sm + td.o_uh) + skh;
+    for (int i = tid; i < n1; i += TT) {
+      double ri = rs[i];
+      if (mode == M_ITER) {
+        ri -= alpha * qs[i];
+        rs[i] = ri;
+        r[a1 + i] = ri;
+      }
+      rr += ri * ri;
+      gd += hs[i] * ri;
+    }
+    if (tid == 0) sky0 = skr;
+  }
   if (nl > 1) {
     __syncthreads();
     const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
-    const double* yc = y0 + (FIRST ? 0 : sky0);
+    const double* yc = y0 + sky0;
     const int a0 = sa0, np = sn1;
     double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
     for (int i = warp; i < np; i += TT / 32) {
@@ -630,9 +637,11 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
       if (lane == 0) yp[i] = y;
     }
   }
+  TRACE(5);
   pdl_trigger();
   if (FIRST) {
     const double2 v = block_sum2<TT>(make_double2(rr, gd));
+    TRACE(6);
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
       if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
@@ -646,6 +655,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
         }
       }
     }
+    TRACE(7);
   }
 }
 

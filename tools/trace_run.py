@@ -25,8 +25,10 @@ L = ctypes.CDLL(%r)
 buf = np.zeros((8, 16), dtype=np.uint64)
 for _ in range(3):
     z = S.apply_R(r); torch.cuda.synchronize()
+x = torch.empty_like(r)
+S.pcg_solve(r, x, rtol=0.0, maxit=40); torch.cuda.synchronize()
 L.msp_debug_trace(buf.ctypes.data)
-names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>'}
+names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>', 4: 'k_tile_up<FIRST>', 5: 'k_tile_up<tier2>'}
 for kid, nm in names.items():
     row = buf[kid].astype(np.int64)
     nz = [i for i in range(16) if row[i]]
