@@ -923,10 +923,12 @@ TierDesc tier_layout(int k0, int nl, int64_t ntiles, const std::vector<int64_t>&
   for (int t = 1; t < nl; ++t) d.o_ki[t] = take((3 * cap[t] + 2) * 8);
   for (int t = 0; t + 1 < nl; ++t) d.o_lo[t] = take((3 * caplo[t] + 2) * 8);
   d.o_n[0] = (k0 > 1) ? take((cap[0] + 2) * 8) : 0;
+  // z, w of an intermediate level overwrite its y, N: the down step of level
+  // k reads y_p, N_p of a child before it writes z_p, w_p (block_solve)
   for (int t = 1; t + 1 < nl; ++t) {
     d.o_n[t] = take(cap[t] * 8);
-    d.o_z[t] = take(cap[t] * 8);
-    d.o_w[t] = take(cap[t] * 8);
+    d.o_z[t] = d.o_y[t];
+    d.o_w[t] = d.o_n[t];
   }
   d.o_z[nl - 1] = take((cap[nl - 1] + 2) * 8);
   d.o_w[nl - 1] = take((cap[nl - 1] + 2) * 8);

@@ -70,8 +70,18 @@ __device__ unsigned long long g_trace[8][16];
       g_trace[TRACE_KID][tag] = t_;                                                                 \
     }                                                                                               \
   } while (0)
+// latest end over all CTAs (slot 15)
+#define TRACE_END()                                                                                 \
+  do {                                                                                              \
+    if (threadIdx.x == 0) {                                                                         \
+      unsigned long long t_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      atomicMax(&g_trace[TRACE_KID][15], t_);                                                       \
+    }                                                                                               \
+  } while (0)
 #else
 #define TRACE(tag) do {} while (0)
+#define TRACE_END() do {} while (0)
 #endif
 #define TRACE_KID 0
 
@@ -367,6 +377,8 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 // Software-pipelined SELL SpMV for slices no wider than MW (fused PCG form):
 // while slice s is gathered and reduced, the slice pointers of s+2 and the
 // column / weight / row vectors of s+1 are already in flight.
+#undef TRACE_KID
+#define TRACE_KID 6
 template <int MW, bool UNIF>
 __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
@@ -379,7 +391,9 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
                                                       double* __restrict__ part, double* __restrict__ scal,
                                                       unsigned int* __restrict__ cnt) {
   // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
+  TRACE(0);
   pdl_wait();
+  TRACE(1);
   if (cnt[C_DONE]) return;
   const double beta = scal[S_BETA];
   const double alpha = scal[S_ALPHA];
@@ -460,6 +474,7 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
       d += pi * acc;
     }
   }
+  TRACE(2);
   pdl_trigger();
   const double bs = block_sum<TPB>(d);
   if (threadIdx.x < 32) {
@@ -473,6 +488,7 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
       }
     }
   }
+  TRACE_END();
 }
 
 // x += alpha p for the last direction (the in-loop updates are deferred into
@@ -657,6 +673,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     }
     TRACE(7);
   }
+  TRACE_END();
 }
 
 // ---------------------------------------------------------- tile down-sweep
@@ -893,6 +910,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
       }
     }
   }
+  TRACE_END();
 }
 
 #undef TRACE_KID
@@ -1601,6 +1619,9 @@ void alloc_solve_workspace(Handle& h) {
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   for (auto f : {(const void*)k_tile_down<true>, (const void*)k_tile_down<false>})
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>, (const void*)k_tile_down<true>,
+                 (const void*)k_tile_down<false>})
+    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)h.coarse_smem));
 }

@@ -29,12 +29,15 @@ x = torch.empty_like(r)
 S.pcg_solve(r, x, rtol=0.0, maxit=40); torch.cuda.synchronize()
 L.msp_debug_trace(buf.ctypes.data)
 names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>', 4: 'k_tile_up<FIRST>', 5: 'k_tile_up<tier2>'}
-for kid, nm in names.items():
+names[6] = 'k_spmv_pipe'
+T0 = min(int(buf[k][0]) for k in names if buf[k][0])
+for kid, nm in sorted(names.items(), key=lambda kv: int(buf[kv[0]][0]) or 1 << 62):
     row = buf[kid].astype(np.int64)
     nz = [i for i in range(16) if row[i]]
     if nz:
         t0 = row[nz[0]]
-        print('TRACE', nm, ' '.join(f'{i}:{(row[i]-t0)/1000:.2f}us' for i in nz))
+        end = f' end={(row[15]-T0)/1000:.2f}us' if row[15] else ''
+        print('TRACE', nm, f'start={(t0-T0)/1000:.2f}us' + end, ' '.join(f'{i}:{(row[i]-t0)/1000:.2f}us' for i in nz if i < 15))
 print('INFO', S.info())
 """ % (ROOT, int(sys.argv[1]) if len(sys.argv) > 1 else 1, lib)
 env = dict(os.environ, MSP_LIB_OVERRIDE=lib)
