@@ -130,6 +130,23 @@ __device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t byte
                : "memory");
 }
 
+// the same with an L2 evict-last policy: the solve's constant arrays
+// (hierarchy pointers, factors) are re-read every iteration and should stay
+// resident in the 126 MB L2 while the streamed vectors pass through it
+__device__ __forceinline__ void tma_1d_keep(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#ifndef MSP_NO_L2KEEP
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
+  tma_1d(dst, src, bytes, bar);
+#endif
+}
+
 // ------------------------------------------------------------ reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -416,8 +433,14 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
 #pragma unroll
     for (int k = 0; k < MW; ++k) {
       if (k < wd) {
+#ifndef MSP_NO_SPMV_CS  // streamed once per iteration: evict-first, so the
+                        // vectors the next kernels re-read stay in L2
+        jc[k] = __ldcs(scol + bb0 + k * 32 + lane);
+        wc[k] = __ldcs(sw + bb0 + k * 32 + lane);
+#else
         jc[k] = scol[bb0 + k * 32 + lane];
         wc[k] = sw[bb0 + k * 32 + lane];
+#endif
       }
     }
     mk = smask[ss];
@@ -447,7 +470,11 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
     if (r < n && !((mk >> lane) & 1u)) {
       q[r] = acc;
       zpout[2 * r + 1] = pi;
+#ifndef MSP_NO_X_CS
+      __stcs(x + r, __ldcs(x + r) + alpha * po);
+#else
       x[r] += alpha * po;
+#endif
       d += pi * acc;
     }
     // next slice's columns / weights / row vectors
@@ -524,6 +551,7 @@ struct LvlPtr {
 // starts at the 16-byte-aligned element at or below lo.  Returns the skew
 // lo - window start (elements).  Called by one thread per segment; the
 // barrier's single arrival comes after every segment's expect_tx.
+template <bool KEEP = false>
 __device__ __forceinline__ int stage_window(uint64_t* bar, char* dst, const void* src, int es, int64_t lo,
                                             int64_t hi) {
   const int64_t m = (es == 4) ? 3 : 1;
@@ -532,7 +560,8 @@ __device__ __forceinline__ int stage_window(uint64_t* bar, char* dst, const void
     const int64_t e0 = (hi + m) & ~m;
     const uint32_t bytes = (uint32_t)((e0 - a0) * es);
     mbar_expect_tx(bar, bytes);
-    tma_1d(dst, (const char*)src + a0 * es, bytes, bar);
+    if (KEEP) tma_1d_keep(dst, (const char*)src + a0 * es, bytes, bar);
+    else tma_1d(dst, (const char*)src + a0 * es, bytes, bar);
   }
   return (int)(lo - a0);
 }
@@ -587,13 +616,13 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     if (nl > 1) {
       sa1 = tstart[(nl - 1) * nt1 + tA];
       sn1 = tstart[(nl - 1) * nt1 + tB] - sa1;
-      skf = stage_window(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
+      skf = stage_window<true>(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
     }
     // FIRST: the level-1 H (constant) and, in PCG iterations, r (last written
     // by the previous iteration's up kernel) are staged before the grid
     // dependency resolves; q after it
     if (FIRST && sn0 > 0) {
-      skh = stage_window(&bar, sm + td.o_uh, H, 8, sa0, (int64_t)sa0 + sn0);
+      skh = stage_window<true>(&bar, sm + td.o_uh, H, 8, sa0, (int64_t)sa0 + sn0);
       if (mode == M_ITER) skr = stage_window(&bar, sm + td.o_uy0, r, 8, sa0, (int64_t)sa0 + sn0);
     }
   }
@@ -719,20 +748,20 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   if (g < m1) {
     const int t = g + 1;
     const int64_t base = lv.cpo[k0 + t - 2];
-    skc[t] = stage_window(&bar, sm + td.o_cp[t], cptr, 4, base + sa[t], base + sa[t] + sn[t] + 1);
+    skc[t] = stage_window<true>(&bar, sm + td.o_cp[t], cptr, 4, base + sa[t], base + sa[t] + sn[t] + 1);
   } else if (g < 2 * m1) {
     const int t = g - m1 + 1;
     const int64_t base = 3 * (lv.off[k0 + t - 1] - n1 + sa[t]);
-    skk[t] = stage_window(&bar, sm + td.o_ki[t], kinv, 8, base, base + 3 * (int64_t)sn[t]);
+    skk[t] = stage_window<true>(&bar, sm + td.o_ki[t], kinv, 8, base, base + 3 * (int64_t)sn[t]);
   } else if (g < 3 * m1) {
     const int t = g - 2 * m1;
     const int64_t lo0 = (int64_t)sa[t] - 2 * (int64_t)sa[t + 1];
     const int64_t lo1 = (int64_t)(sa[t] + sn[t]) - 2 * (int64_t)(sa[t + 1] + sn[t + 1]);
     const int64_t base = 3 * lv.lo[k0 + t - 1];
-    skl[t] = stage_window(&bar, sm + td.o_lo[t], lof, 8, base + 3 * lo0, base + 3 * lo1);
+    skl[t] = stage_window<true>(&bar, sm + td.o_lo[t], lof, 8, base + 3 * lo0, base + 3 * lo1);
   } else if (!FIRST && g == 3 * m1) {
     const int64_t base = lv.off[k0 - 1];
-    skn0 = stage_window(&bar, sm + td.o_n[0], Nsub, 8, base + sa[0], base + sa[0] + sn[0]);
+    skn0 = stage_window<true>(&bar, sm + td.o_n[0], Nsub, 8, base + sa[0], base + sa[0] + sn[0]);
   }
   TRACE(1);
   pdl_wait();
@@ -1008,22 +1037,22 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   if (g < m1) {
     const int t = g + 1;
     const int64_t base = lv.cpo[Kc + t - 2];
-    skc[t] = stage_window(&bar, sm + cd.o_cp[t], cptr, 4, base, base + lv.n[Kc + t - 1] + 1);
+    skc[t] = stage_window<true>(&bar, sm + cd.o_cp[t], cptr, 4, base, base + lv.n[Kc + t - 1] + 1);
   } else if (g < 2 * m1) {
     const int t = g - m1 + 1;
     const int64_t base = 3 * (lv.off[Kc + t - 1] - n1);
-    skk[t] = stage_window(&bar, sm + cd.o_ki[t], kinv, 8, base, base + 3 * lv.n[Kc + t - 1]);
+    skk[t] = stage_window<true>(&bar, sm + cd.o_ki[t], kinv, 8, base, base + 3 * lv.n[Kc + t - 1]);
   } else if (g < 3 * m1) {
     const int t = g - 2 * m1;
     const int64_t base = 3 * lv.lo[Kc + t - 1];
-    skl[t] = stage_window(&bar, sm + cd.o_lo[t], lof, 8, base, base + 3 * (lv.n[Kc + t - 1] - 2 * lv.n[Kc + t]));
+    skl[t] = stage_window<true>(&bar, sm + cd.o_lo[t], lof, 8, base, base + 3 * (lv.n[Kc + t - 1] - 2 * lv.n[Kc + t]));
   } else if (g < 3 * m1 + nl) {
     const int t = g - 3 * m1;
     const int64_t base = lv.off[Kc + t - 1];
-    skn[t] = stage_window(&bar, sm + cd.o_n[t], Nsub, 8, base, base + lv.n[Kc + t - 1]);
+    skn[t] = stage_window<true>(&bar, sm + cd.o_n[t], Nsub, 8, base, base + lv.n[Kc + t - 1]);
   } else if (g == 3 * m1 + nl && cd.stage_pinv) {
     const int64_t nt = lv.n[L - 1];
-    skp = stage_window(&bar, sm + cd.o_pinv, pinv_g, 8, 0, nt * nt);
+    skp = stage_window<true>(&bar, sm + cd.o_pinv, pinv_g, 8, 0, nt * nt);
   }
   TRACE(1);
   pdl_wait();

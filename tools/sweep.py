@@ -44,7 +44,7 @@ def main():
             if k == "LIB":  # a library variant built with extra nvcc flags, e.g. LIB=-DMSP_TT=128
                 from paper_2207_07847_b200 import build as B
                 sys.path.insert(0, ROOT)
-                path = os.path.join(ROOT, "build_variant_" + v.replace("-D", "").replace("=", "_") + ".so")
+                path = os.path.join(ROOT, "build_variant_" + v.replace("-D", "").replace("=", "_").replace(",", "+") + ".so")
                 B.build(force=True, extra=v.split(","), lib=path)
                 env["MSP_LIB_OVERRIDE"] = path
             else:
