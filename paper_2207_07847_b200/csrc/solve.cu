@@ -41,6 +41,9 @@ constexpr int TPB = 256;      // SpMV and per-node kernels
 #define MSP_TT 128
 #endif
 constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
+#ifndef MSP_FLAT_G
+#define MSP_FLAT_G 4
+#endif
 #ifndef MSP_CT
 #define MSP_CT 1024
 #endif
@@ -674,12 +677,23 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     const double* yc = y0 + sky0;
     const int a0 = sa0, np = sn1;
     double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
-    for (int i = warp; i < np; i += TT / 32) {
-      const int c0 = f[i] - a0, c1 = f[i + 1] - a0;
-      double y = 0.0;
-      for (int c = c0 + lane; c < c1; c += 32) y += yc[c];
-      y = warp_sum(y);
-      if (lane == 0) yp[i] = y;
+    // FG lanes per level-k1 node, two partial sums per lane, then a
+    // butterfly over the group (fixed order)
+    constexpr int FG = MSP_FLAT_G;
+    const int sub = tid & (FG - 1);
+    for (int base = 0; base < np; base += TT / FG) {  // block-uniform trip count
+      const int i = base + tid / FG;
+      double ya = 0.0, yb = 0.0;
+      if (i < np) {
+        const int c0 = f[i] - a0, c1 = f[i + 1] - a0;
+        int c = c0 + sub;
+        for (; c + FG < c1; c += 2 * FG) { ya += yc[c]; yb += yc[c + FG]; }
+        if (c < c1) ya += yc[c];
+      }
+      double y = ya + yb;
+#pragma unroll
+      for (int o = FG / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (sub == 0 && i < np) yp[i] = y;
     }
   }
   TRACE(5);
@@ -873,6 +887,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   double rz = 0.0;
   for (int t = nl - 2; t >= 1; --t) {  // child level k = k0+t, parent level k+1
     __syncthreads();
+    TRACE(6 + t);
     const int* cp = SMP(const int, tb[t + 1].cp);
     const double* ki = SMP(const double, tb[t + 1].ki);
     const double* zp = SMP(const double, tb[t + 1].z);
@@ -1111,6 +1126,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   }
   // ---- top solve
   __syncthreads();
+  TRACE(7);
   const int ntop = tb[nl - 1].cnt;
   const double* yt = SMP(const double, tb[nl - 1].y);
   const double* Nt = SMP(const double, tb[nl - 1].nn);
@@ -1121,6 +1137,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     ysum = v.x;
     gd = v.y;
   }
+  TRACE(8);
   const double rho = lv.c_sum * ysum / lv.n_tilde;
   double* tt = reinterpret_cast<double*>(sm + cd.o_tt);
   for (int i = tid; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
@@ -1135,7 +1152,9 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     zt[i] = zi;
     nz += Nt[i] * zi;
   }
+  TRACE(9);
   nz = block_sum<CT>(nz);
+  TRACE(10);
   if (tid == 0 && mode != M_COLUMN) scal[S_SHIFT] = rho;
   const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
   double rz = 0.0;
