@@ -61,11 +61,16 @@ def test_dist_solve_world1_matches_oracle(pg, name, make):
     ref = PC.pcg(lambda v: L @ v, b, PR.msp(sysm), 1e-8, 20000)
     single = S.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
     assert out["converged"] == 1 and ref.converged
-    assert abs(out["iterations"] - single["iterations"]) <= 2, (out["iterations"], single["iterations"])
     from test_gpu_parity import iteration_band
+    # the partitioned and the single-GPU solve sum their dots in different
+    # orders: two equally exact runs, so they agree within the rounding band
+    # of reading R11 (>= 2), as each does with the oracle
     d = abs(out["iterations"] - ref.iterations)
-    if d > 2:
-        assert d <= iteration_band(L, b, sysm, ref.iterations), (name, out["iterations"], ref.iterations)
+    ds = abs(out["iterations"] - single["iterations"])
+    if max(d, ds) > 2:
+        band = iteration_band(L, b, sysm, ref.iterations)
+        assert d <= band, (name, out["iterations"], ref.iterations, band)
+        assert ds <= band, (name, out["iterations"], single["iterations"], band)
     x = out["x"].cpu().numpy()
     e = x - ref.x
     e -= e.mean()
