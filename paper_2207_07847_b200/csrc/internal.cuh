@@ -144,6 +144,7 @@ struct Handle {
   DBuf<double> Mco;
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
+  unsigned fuse_grid = 0;  // grid of the fused SpMV + first-tier up kernel (0: not used)
 
   // ---- PEGP (built lazily on first use, pegp.cu)
   bool pegp_ready = false;

@@ -30,6 +30,7 @@ S.pcg_solve(r, x, rtol=0.0, maxit=40); torch.cuda.synchronize()
 L.msp_debug_trace(buf.ctypes.data)
 names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>', 4: 'k_tile_up<FIRST>', 5: 'k_tile_up<tier2>'}
 names[6] = 'k_spmv_pipe'
+names[7] = 'k_spmv_up'
 T0 = min(int(buf[k][0]) for k in names if buf[k][0])
 for kid, nm in sorted(names.items(), key=lambda kv: int(buf[kv[0]][0]) or 1 << 62):
     row = buf[kid].astype(np.int64)
