@@ -68,9 +68,14 @@ __device__ unsigned long long g_trace[8][16];
 #define TRACE(tag)                                                                                  \
   do {                                                                                              \
     if (threadIdx.x == 0 && blockIdx.x == 0) {                                                      \
-      unsigned long long t_;                                                                        \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
-      g_trace[TRACE_KID][tag] = t_;                                                                 \
+      if ((tag) == 0) {                                                                             \
+        unsigned long long t_;                                                                      \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+        g_trace[TRACE_KID][0] = t_;                                                                 \
+        g_trace[TRACE_KID][14] = clock64();                                                         \
+      } else {                                                                                      \
+        g_trace[TRACE_KID][tag] = clock64(); /* SM cycles; slot 14 = cycles at tag 0 */            \
+      }                                                                                             \
     }                                                                                               \
   } while (0)
 // latest end over all CTAs (slot 15)
@@ -231,11 +236,19 @@ __device__ __forceinline__ bool warp_last_block(unsigned int* counter) {
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
-// fixed-order sum of partials[0..n) by one warp (all lanes get the result)
+// fixed-order sum of partials[0..n) by one warp (all lanes get the result);
+// four independent chains so the L2 loads overlap
 __device__ __forceinline__ double warp_sum_partials(const double* part, int64_t n) {
-  double v = 0.0;
-  for (int64_t i = threadIdx.x & 31; i < n; i += 32) v += __ldcg(part + i);
-  return warp_sum(v);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = threadIdx.x & 31;
+  for (; i + 96 < n; i += 128) {
+    a0 += __ldcg(part + i);
+    a1 += __ldcg(part + i + 32);
+    a2 += __ldcg(part + i + 64);
+    a3 += __ldcg(part + i + 96);
+  }
+  for (; i < n; i += 32) a0 += __ldcg(part + i);
+  return warp_sum((a0 + a1) + (a2 + a3));
 }
 
 // Exact solve of one aggregate of T~: children [s0, s1) (matched pair s0,
@@ -253,6 +266,7 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
     return;
   }
   double au = tu, av = tv;
+  #pragma unroll 1
   for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     au += C(p, 0) * tx;
@@ -261,6 +275,7 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
   const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
   { const double z = zb + zu; ef(s0, z, z + wbm); }
   { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
+  #pragma unroll 1
   for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     const double zx = C(p, 2) * tx + C(p, 0) * zu + C(p, 1) * zv;
@@ -705,10 +720,11 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
       if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
       if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
         const double tot = warp_sum_partials(part_rr + tile0, gridDim.x);
+        const double tgd = warp_sum_partials(part_gd + tile0, gridDim.x);  // (H, r) for the coarse kernel
         if (dist) {  // local totals; k_dist_finish runs after the all-reduce
-          const double tgd = warp_sum_partials(part_gd + tile0, gridDim.x);
           if (tid == 0) { scal[S_RR] = tot; scal[S_GD] = tgd; cnt[C_UPD] = 0; }
         } else if (tid == 0) {
+          scal[S_GD] = tgd;
           finish_rr(tot, scal, cnt, mode);
           cnt[C_UPD] = 0;
         }
@@ -954,7 +970,9 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_up(int64_t n, int64_t nslices, 
     if (tid == 0) { part_rr[blockIdx.x] = v.x; part_gd[blockIdx.x] = v.y; }
     if (warp_last_block(&cnt[C_UPD])) {
       const double tot = warp_sum_partials(part_rr, gridDim.x);
+      const double tgd = warp_sum_partials(part_gd, gridDim.x);
       if (tid == 0) {
+        scal[S_GD] = tgd;
         finish_rr(tot, scal, cnt, M_ITER);
         cnt[C_UPD] = 0;
       }
@@ -1113,15 +1131,29 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     double* yp = SMP(double, tb[t].y);
     double* np = SMP(double, tb[t].nn);
     const int ac = tb[t - 1].a, npar = tb[t].cnt;
-    for (int i = tid; i < npar; i += TT) {
-      const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
-      double y = 0.0, N = 1.0;
-      for (int c = c0; c < c1; ++c) {
-        y += yc[c];
-        N += nc ? nc[c] : 1.0;
+    if (nc) {
+      #pragma unroll 1
+      for (int i = tid; i < npar; i += TT) {
+        const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
+        double y = 0.0, N = 1.0;
+        #pragma unroll 1
+        for (int c = c0; c < c1; ++c) {
+          y += yc[c];
+          N += nc[c];
+        }
+        yp[i] = y;
+        np[i] = N;
       }
-      yp[i] = y;
-      np[i] = N;
+    } else {  // level-1 children: N = 1 each
+      #pragma unroll 1
+      for (int i = tid; i < npar; i += TT) {
+        const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
+        double y = yc[c0] + yc[c0 + 1];  // every aggregate has its matched pair
+        #pragma unroll 1
+        for (int c = c0 + 2; c < c1; ++c) y += yc[c];
+        yp[i] = y;
+        np[i] = (double)(1 + c1 - c0);
+      }
     }
   }
   TRACE(4);
@@ -1143,6 +1175,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     double* wc = SMP(double, tb[t].w);
     const int ac = tb[t].a, npar = tb[t + 1].cnt;
     const double ckk = tb[t].ck;
+    #pragma unroll 1
     for (int i = tid; i < npar; i += TT) {
       const int lb = -3 * (2 * i + 2);
       block_solve(
@@ -1166,6 +1199,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     const int zs = (mode_in & M_ZS2) ? 2 : 1;
     double* zg = FIRST ? zout + zs * ac : Zg + lv.off[k0 - 1] + ac;
     double* wg = Wg + lv.off[k0 - 1] + ac;
+    #pragma unroll 1
     for (int i = tid; i < npar; i += TT) {
       const int lb = -3 * (2 * i + 2);
       if (FIRST)
@@ -1262,12 +1296,180 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
 }
 
 // --------------------------------------------------------- coarse kernel
+// Levels Kc..L of the coarse kernel when the top has <= 32 nodes.  Level t
+// (n_{Kc+t} nodes, one per thread) runs on its first W(t) = ceil(n/32) warps
+// only; the barrier before a level spans exactly the warps of the larger of
+// the two levels it separates (a named barrier, __syncwarp for one warp), so
+// the small upper levels cost a warp-level sync instead of a 32-warp one.  The
+// top solve runs on warp 0.  Level Kc goes straight to global memory.
+// Barrier ids: 1 for the up sweep (its warp sets only shrink, so every warp
+// of an instance has left the previous one); one id per down level (2 + t),
+// because a warp that joins the down sweep late arrives at its first barrier
+// while the others are still levels above.
+__device__ __forceinline__ void named_sync(int id, int nw) {
+  if (nw == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nw * 32) : "memory");
+}
+
+#undef TRACE_KID
+#define TRACE_KID 1
+__device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, char* sm, const double* __restrict__ pinv,
+                                           double* __restrict__ Zg, double* __restrict__ Wg,
+                                           double* __restrict__ zout, double* __restrict__ scal, double gd,
+                                           int mode_in, int o_tt) {
+  constexpr int NW = CT / 32;
+  const int mode = mode_in & 15;
+  const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ double srho;
+  auto W = [&](int t) {
+    const int c = (int)((lv.n[Kc + t - 1] + 31) >> 5);
+    return c < 1 ? 1 : (c > NW ? NW : c);
+  };
+  __syncthreads();  // pointer table and staged segments
+  // ---- up: level t on warps [0, W(t))
+  for (int t = 1; t < nl; ++t) {
+    if (t >= 2) {
+      const int wp = W(t - 1);
+      if (warp >= wp) break;
+      named_sync(1, wp);
+    }
+    if (t <= 7) TRACE(6 + t);
+    const int wt = W(t);
+    if (warp < wt) {
+      const int* cp = SMP(const int, tb[t].cp);
+      const double* yc = SMP(const double, tb[t - 1].y);
+      double* yp = SMP(double, tb[t].y);
+      const int np = tb[t].cnt;
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        double y = 0.0;
+        const int c1 = cp[i + 1];
+        #pragma unroll 1
+        for (int c = cp[i]; c < c1; ++c) y += yc[c];
+        yp[i] = y;
+      }
+    }
+  }
+  // ---- top solve (warp 0)
+  double rz = 0.0;
+  const int ntop = tb[nl - 1].cnt;
+  if (warp == 0) {
+    __syncwarp();
+    const double* yt = SMP(const double, tb[nl - 1].y);
+    const double* Nt = SMP(const double, tb[nl - 1].nn);
+    double ysum = 0.0;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) ysum += yt[i];
+    ysum = warp_sum(ysum);
+    gd = warp_sum(gd);
+    const double rho = lv.c_sum * ysum / lv.n_tilde;
+    double* tt = reinterpret_cast<double*>(sm + o_tt);
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
+    __syncwarp();
+    double* zt = SMP(double, tb[nl - 1].z);
+    double* wt = SMP(double, tb[nl - 1].w);
+    double nz = 0.0;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) {
+      double zi = 0.0;
+      #pragma unroll 1
+      for (int j = 0; j < ntop; ++j) zi += pinv[i * ntop + j] * tt[j];
+      zt[i] = zi;
+      nz += Nt[i] * zi;
+    }
+    nz = warp_sum(nz);
+    const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) {
+      const double z = zt[i] - m;
+      zt[i] = z;
+      wt[i] = z;
+      if (L == 1) {
+        rz += yt[i] * z;
+        zout[((mode_in & M_ZS2) ? 2 : 1) * i] = z;
+      } else if (nl == 1) {  // the top is level Kc: to global
+        if (mode == M_COLUMN) {
+          Zg[(int64_t)blockIdx.x * 2 * ntop + i] = z;
+          Zg[(int64_t)blockIdx.x * 2 * ntop + ntop + i] = z;
+        } else {
+          Zg[lv.off[Kc - 1] + i] = z;
+          Wg[lv.off[Kc - 1] + i] = z;
+        }
+      }
+    }
+    if (lane == 0) {
+      srho = rho;
+      if (mode != M_COLUMN) scal[S_SHIFT] = rho;
+    }
+    __syncwarp();
+  }
+  TRACE(5);
+  // ---- down: level t on warps [0, W(t)) (W grows as t falls)
+  const double negmu = lv.negmu;
+  for (int t = nl - 2; t >= 0; --t) {
+    const int wt = W(t);
+    if (warp >= wt) continue;
+    named_sync(2 + t, wt);
+    const double rho = srho;
+    const int* cp = SMP(const int, tb[t + 1].cp);
+    const double* ki = SMP(const double, tb[t + 1].ki);
+    const double* zp = SMP(const double, tb[t + 1].z);
+    const double* wp = SMP(const double, tb[t + 1].w);
+    const double* lo = SMP(const double, tb[t].lo);
+    const double* yc = SMP(const double, tb[t].y);
+    const double* nc = SMP(const double, tb[t].nn);
+    double* zc = SMP(double, tb[t].z);
+    double* wc = SMP(double, tb[t].w);
+    const double ckk = tb[t].ck;
+    const int np = tb[t + 1].cnt;
+    const int nk = tb[t].cnt;
+    if (t > 0) {
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zc[p] = z; wc[p] = w; });
+      }
+    } else if (Kc == 1) {  // level-1 output and (r, R r)
+      const int zs = (mode_in & M_ZS2) ? 2 : 1;
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return yc[p] - rho; },
+            [&](int p, double z, double w) { rz += yc[p] * w; zout[zs * p] = w; });
+      }
+    } else {  // level Kc to global: Z, W (or column blockIdx.x of the GEMV map)
+      double* zg = (mode == M_COLUMN) ? Zg + (int64_t)blockIdx.x * 2 * nk : Zg + lv.off[Kc - 1];
+      double* wg = (mode == M_COLUMN) ? zg + nk : Wg + lv.off[Kc - 1];
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zg[p] = z; wg[p] = w; });
+      }
+    }
+  }
+  TRACE(6);
+  pdl_trigger();
+  if (Kc == 1) {
+    rz = block_sum<CT>(rz);
+    if (tid == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
+  }
+}
+
 // Single CTA: levels Kc..L up-sweep, the top solve, levels L..Kc down-sweep,
 // everything staged in / computed into shared memory (layout: CoarseDesc).
 // When Kc == 1 it also produces the level-1 output and (r, R r).
 #undef TRACE_KID
 #define TRACE_KID 1
-__global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, const __grid_constant__ CoarseDesc cd,
+__global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, const __grid_constant__ CoarseDesc cd,
                                                const int32_t* __restrict__ cptr, const double* __restrict__ kinv,
                                                const double* __restrict__ lof, const double* __restrict__ Nsub,
                                                const double* __restrict__ pinv_g, const double* __restrict__ y0src,
@@ -1282,11 +1484,20 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   __shared__ int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
   __shared__ int sky0, skp, sdone;
   __shared__ LvlPtr tb[MAXT + 8];
-  const int L = lv.L, Kc = lv.Kc, nl = cd.nl, tid = threadIdx.x;
-  const int64_t n1 = lv.n[0];
+  // the level table is read level by level; a single CTA would take a cold
+  // constant-cache miss at nearly every level, so it is copied to shared
+  // memory once, all words in parallel
+  __shared__ __align__(16) Lv slv;
+  static_assert(sizeof(Lv) % 8 == 0, "Lv copied as 8-byte words");
+  for (int i = threadIdx.x; i < (int)(sizeof(Lv) / 8); i += CT)
+    reinterpret_cast<uint64_t*>(&slv)[i] = reinterpret_cast<const uint64_t*>(&lv_p)[i];
+  const Lv& lv = slv;
+  const int tid = threadIdx.x;
   TRACE(0);
   if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
+  const int L = lv.L, Kc = lv.Kc, nl = cd.nl;
+  const int64_t n1 = lv.n[0];
   // segments, one per warp (g = lane * 32 + warp): [0, nl-1) child pointers,
   // [nl-1, 2nl-2) factors, [2nl-2, 3nl-3) leftover coefficients,
   // [3nl-3, 4nl-3) subtree sizes, 4nl-3 the top pseudo-inverse; after the
@@ -1327,12 +1538,25 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   }
   __syncthreads();
   if (tid == 0) mbar_arrive(&bar);
+  // small top (<= 32 nodes): the levels run on as many warps as they have
+  // nodes for, the top solve on warp 0 (so gdot is summed there)
+#ifndef MSP_NO_SMALLTOP
+  const bool small_top = lv.n[L - 1] <= 32 && nl <= 14;
+#else
+  const bool small_top = false;
+#endif
   double gd = 0.0;
   if (mode == M_COLUMN) {
     if (tid == 0) gd = ((int64_t)blockIdx.x == lv.n[Kc - 1]) ? 1.0 : 0.0;
-  } else if (dist) {
-    if (tid == 0) gd = scal[S_GD];  // all-reduced by the caller
-  } else if (!done) {
+  } else if (dist || mode != M_APPLY) {
+    // summed by the up kernel's last CTA (all-reduced by the caller if dist)
+    if (tid == 0 && !done) gd = scal[S_GD];
+  } else if (small_top) {  // apply_R: the partials are summed here (warp 0 holds gdot)
+    if (tid < 32) {
+      const double t = warp_sum_partials(part_gd, npart);
+      gd = (tid == 0) ? t : 0.0;
+    }
+  } else {
     for (int i = tid; i < npart; i += CT) gd += __ldcg(part_gd + i);
   }
   mbar_wait(&bar, 0);
@@ -1354,6 +1578,11 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     e.ck = lv.ck[Kc + t];
     tb[t] = e;
   }
+  if (small_top) {
+    const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
+    coarse_levels(lv, tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, cd.o_tt);
+    return;
+  }
   // ---- up
   for (int t = 1; t < nl; ++t) {  // child level Kc+t-1, parent Kc+t
     __syncthreads();
@@ -1361,9 +1590,11 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     const double* yc = SMP(const double, tb[t - 1].y);
     double* yp = SMP(double, tb[t].y);
     const int np = tb[t].cnt;
+    #pragma unroll 1
     for (int i = tid; i < np; i += CT) {
       double y = 0.0;
       const int c1 = cp[i + 1];
+      #pragma unroll 1
       for (int c = cp[i]; c < c1; ++c) y += yc[c];
       yp[i] = y;
     }
@@ -1375,6 +1606,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   const double* yt = SMP(const double, tb[nl - 1].y);
   const double* Nt = SMP(const double, tb[nl - 1].nn);
   double ysum = 0.0;
+  #pragma unroll 1
   for (int i = tid; i < ntop; i += CT) ysum += yt[i];
   {
     const double2 v = block_sum2<CT>(make_double2(ysum, gd));
@@ -1384,14 +1616,17 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   TRACE(8);
   const double rho = lv.c_sum * ysum / lv.n_tilde;
   double* tt = reinterpret_cast<double*>(sm + cd.o_tt);
+  #pragma unroll 1
   for (int i = tid; i < ntop; i += CT) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
   __syncthreads();
   const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
   double* zt = SMP(double, tb[nl - 1].z);
   double* wt = SMP(double, tb[nl - 1].w);
   double nz = 0.0;
+  #pragma unroll 1
   for (int i = tid; i < ntop; i += CT) {
     double zi = 0.0;
+    #pragma unroll 1
     for (int j = 0; j < ntop; ++j) zi += pinv[i * ntop + j] * tt[j];
     zt[i] = zi;
     nz += Nt[i] * zi;
@@ -1402,6 +1637,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
   if (tid == 0 && mode != M_COLUMN) scal[S_SHIFT] = rho;
   const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
   double rz = 0.0;
+  #pragma unroll 1
   for (int i = tid; i < ntop; i += CT) {
     const double z = zt[i] - m;
     zt[i] = z;
@@ -1425,6 +1661,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv, co
     const double ckk = tb[t].ck;
     const bool out1 = (Kc + t == 1);
     const int np = tb[t + 1].cnt;
+    #pragma unroll 1
     for (int i = tid; i < np; i += CT) {
       const int lb = -3 * (2 * i + 2);
       block_solve(

@@ -11,7 +11,7 @@ from paper_2207_07847_b200 import build as B  # noqa: E402
 lib = os.path.join(ROOT, "build_trace_libmsp.so")
 B.build(force=True, extra=["-DMSP_TRACE"], lib=lib)
 code = r"""
-import sys, torch
+import os, sys, torch
 sys.path.insert(0, %r)
 import paper_2207_07847_b200 as M
 from inputs import graphs as G
@@ -38,7 +38,10 @@ for kid, nm in sorted(names.items(), key=lambda kv: int(buf[kv[0]][0]) or 1 << 6
     if nz:
         t0 = row[nz[0]]
         end = f' end={(row[15]-T0)/1000:.2f}us' if row[15] else ''
-        print('TRACE', nm, f'start={(t0-T0)/1000:.2f}us' + end, ' '.join(f'{i}:{(row[i]-t0)/1000:.2f}us' for i in nz if i < 15))
+        # tags >= 1 are SM clock cycles (slot 14 = cycles at tag 0), at the bench clock
+        ghz = float(os.environ.get('SM_GHZ', '1.965'))
+        print('TRACE', nm, f'start={(t0-T0)/1000:.2f}us' + end,
+              ' '.join(f'{i}:{(row[i]-row[14])/ghz/1000:.2f}us' for i in nz if 0 < i < 14))
 print('INFO', S.info())
 """ % (ROOT, int(sys.argv[1]) if len(sys.argv) > 1 else 1, lib)
 env = dict(os.environ, MSP_LIB_OVERRIDE=lib)
