@@ -41,6 +41,9 @@ constexpr int TPB = 256;      // SpMV and per-node kernels
 #define MSP_TT 128
 #endif
 constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
+#ifndef MSP_PF_DIST
+#define MSP_PF_DIST 1
+#endif
 #ifndef MSP_FLAT_G
 #define MSP_FLAT_G 4
 #endif
@@ -153,6 +156,11 @@ __device__ __forceinline__ void tma_1d_keep(void* dst, const void* src, uint32_t
 #else
   tma_1d(dst, src, bytes, bar);
 #endif
+}
+
+// bulk L2 prefetch of a 16-byte aligned range (no registers, no completion)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // ------------------------------------------------------------ reductions
@@ -427,6 +435,15 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
                                                       unsigned int* __restrict__ cnt) {
   // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
   TRACE(0);
+#ifndef MSP_NO_PF_PRE
+  if (UNIF && (threadIdx.x & 31) == 0) {  // constant streams of the first slices, before the dependency
+    const int64_t w0 = (blockIdx.x * (int64_t)TPB + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * TPB) >> 5;
+    for (int64_t sp = w0; sp < nslices && sp <= w0 + nw; sp += nw) {
+      l2_prefetch(scol + sp * 32 * MW, 32 * MW * 4);
+      l2_prefetch(sw + sp * 32 * MW, 32 * MW * 8);
+    }
+  }
+#endif
   pdl_wait();
   TRACE(1);
   if (cnt[C_DONE]) return;
@@ -467,6 +484,17 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
   if (s < nslices) load_B(s, b0, b1);
   while (s < nslices) {
     const int64_t s1 = s + nwarps;
+#if MSP_PF_DIST > 0
+    if (UNIF && lane == 0) {  // the streams of slice s + PF * nwarps into L2
+      const int64_t sp = s + MSP_PF_DIST * nwarps;
+      if ((sp + 1) * 32 <= n) {
+        l2_prefetch(scol + sp * 32 * MW, 32 * MW * 4);
+        l2_prefetch(sw + sp * 32 * MW, 32 * MW * 8);
+        l2_prefetch(zp + sp * 32, 32 * 16);
+        l2_prefetch(x + sp * 32, 32 * 8);
+      }
+    }
+#endif
     int64_t n0 = 0, n1 = 0;
     if (UNIF) { n0 = s1 * 32 * MW; n1 = n0 + 32 * MW; }
     else if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
