@@ -90,9 +90,23 @@ __device__ unsigned long long g_trace[8][16];
       atomicMax(&g_trace[TRACE_KID][15], t_);                                                       \
     }                                                                                               \
   } while (0)
+// per-phase SM cycles summed over every CTA (thread 0): PHASE(k) adds the
+// cycles since the previous PHASE call (or PHASE_START) to slot k
+__device__ unsigned long long g_phase[8][16];
+#define PHASE_START() long long ph_t_ = clock64()
+#define PHASE(k)                                                                                    \
+  do {                                                                                              \
+    if (threadIdx.x == 0) {                                                                         \
+      const long long t_ = clock64();                                                               \
+      atomicAdd(&g_phase[TRACE_KID][k], (unsigned long long)(t_ - ph_t_));                          \
+      ph_t_ = t_;                                                                                   \
+    }                                                                                               \
+  } while (0)
 #else
 #define TRACE(tag) do {} while (0)
 #define TRACE_END() do {} while (0)
+#define PHASE_START() do {} while (0)
+#define PHASE(k) do {} while (0)
 #endif
 #define TRACE_KID 0
 
@@ -655,6 +669,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TRACE(0);
+  PHASE_START();
   if (tid == 0) {
     mbar_init(&bar, 1);
     sa0 = tstart[tA];
@@ -673,8 +688,10 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     }
   }
   TRACE(1);
+  PHASE(0);
   pdl_wait();
   TRACE(2);
+  PHASE(1);
   if (tid == 0) {
     sdone = (mode == M_ITER) ? (int)cnt[C_DONE] : 0;
     salpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
@@ -695,6 +712,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   TRACE(3);
   mbar_wait(&bar, 0);
   TRACE(4);
+  PHASE(2);
   if (done) return;
   if (FIRST) {  // level-1 update from shared memory; r_new in place of r (it is y_1)
     const double alpha = salpha;
@@ -714,6 +732,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     }
     if (tid == 0) sky0 = skr;
   }
+  PHASE(3);
   if (nl > 1) {
     __syncthreads();
     const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
@@ -740,10 +759,12 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     }
   }
   TRACE(5);
+  PHASE(4);
   pdl_trigger();
   if (FIRST) {
     const double2 v = block_sum2<TT>(make_double2(rr, gd));
     TRACE(6);
+    PHASE(5);
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
       if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
@@ -759,7 +780,11 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
       }
     }
     TRACE(7);
+    PHASE(6);
   }
+#ifdef MSP_TRACE
+  if (threadIdx.x == 0) atomicAdd(&g_phase[TRACE_KID][15], 1ull);
+#endif
   TRACE_END();
 }
 
@@ -1037,6 +1062,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   TRACE(0);
+  PHASE_START();
   if (tid == 0) mbar_init(&bar, 1);
   if (tid < nl) {
     const int a = tstart[tid * nt1 + tile];
@@ -1068,8 +1094,10 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     skn0 = stage_window<true>(&bar, sm + td.o_n[0], Nsub, 8, base + sa[0], base + sa[0] + sn[0]);
   }
   TRACE(1);
+  PHASE(0);
   pdl_wait();
   TRACE(2);
+  PHASE(1);
   // dynamic segments (y_k0, z and w at level k1) go out at once; the done
   // flag and rho are read alongside (a finished solve only wastes the copies)
   if (tid == 0) {
@@ -1131,6 +1159,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   if (tid == 0) mbar_arrive(&bar);
   mbar_wait(&bar, 0);
   TRACE(3);
+  PHASE(2);
   if (done) return;
 
   // per-level pointer table (one thread per level), so every phase starts
@@ -1185,6 +1214,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     }
   }
   TRACE(4);
+  PHASE(3);
   // ---- down: levels k1-1 .. k0+1 in shared memory, then level k0 out
   const double rho = srho;
   const double negmu = lv.negmu;
@@ -1215,6 +1245,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   }
   {
     __syncthreads();
+    PHASE(4);
     const int* cp = SMP(const int, tb[1].cp);
     const double* ki = SMP(const double, tb[1].ki);
     const double* zp = SMP(const double, tb[1].z);
@@ -1245,6 +1276,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     }
   }
   TRACE(5);
+  PHASE(5);
   pdl_trigger();
   if (FIRST) {
     rz = block_sum<TT>(rz);
@@ -1260,6 +1292,10 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
       }
     }
   }
+  PHASE(6);
+#ifdef MSP_TRACE
+  if (threadIdx.x == 0) atomicAdd(&g_phase[TRACE_KID][15], 1ull);
+#endif
   TRACE_END();
 }
 
@@ -2402,6 +2438,14 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
 #ifdef MSP_TRACE
 extern "C" int msp_debug_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, msp::g_trace, sizeof(msp::g_trace)) == cudaSuccess ? 0 : -2;
+}
+extern "C" int msp_debug_phase(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, msp::g_phase, sizeof(msp::g_phase)) != cudaSuccess) return -2;
+  if (reset) {
+    static unsigned long long z[8][16] = {};
+    if (cudaMemcpyToSymbol(msp::g_phase, z, sizeof(z)) != cudaSuccess) return -2;
+  }
+  return 0;
 }
 #endif
 

@@ -26,7 +26,15 @@ buf = np.zeros((8, 16), dtype=np.uint64)
 for _ in range(3):
     z = S.apply_R(r); torch.cuda.synchronize()
 x = torch.empty_like(r)
+ph = np.zeros((8, 16), dtype=np.uint64)
+L.msp_debug_phase(ph.ctypes.data, 1)
 S.pcg_solve(r, x, rtol=0.0, maxit=40); torch.cuda.synchronize()
+L.msp_debug_phase(ph.ctypes.data, 0)
+for kid, nm in {2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>', 4: 'k_tile_up<FIRST>', 5: 'k_tile_up<tier2>'}.items():
+    c = int(ph[kid][15])
+    if c:
+        ghz = float(os.environ.get('SM_GHZ', '1.965'))
+        print('PHASE', nm, 'ctas', c, ' '.join(f'{k}:{ph[kid][k] / c / ghz / 1000:.2f}us' for k in range(8) if ph[kid][k]))
 L.msp_debug_trace(buf.ctypes.data)
 names = {1: 'k_coarse', 2: 'k_tile_down<FIRST>', 3: 'k_tile_down<tier2>', 4: 'k_tile_up<FIRST>', 5: 'k_tile_up<tier2>'}
 names[6] = 'k_spmv_pipe'
@@ -46,7 +54,7 @@ print('INFO', S.info())
 """ % (ROOT, int(sys.argv[1]) if len(sys.argv) > 1 else 1, lib)
 env = dict(os.environ, MSP_LIB_OVERRIDE=lib)
 out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-lines = [l for l in out.stdout.splitlines() if l.startswith("TRACE") or l.startswith("INFO")]
+lines = [l for l in out.stdout.splitlines() if l.startswith("TRACE") or l.startswith("INFO") or l.startswith("PHASE")]
 print(out.stderr[-2000:])
 # last apply only: group by kernel, print deltas
 last = lines[-(len(lines) // 3 + 1):]
