@@ -13,6 +13,8 @@
 
 namespace msp {
 
+constexpr int HEAVY_AGG = 64;
+
 enum { PC_SPMV = 0, PC_TILE_UP, PC_MID_UP, PC_COARSE, PC_MID_DOWN, PC_TILE_DOWN, PC_UNUSED6, PC_UNUSED7 };
 
 // ---------------------------------------------------------------- errors
@@ -97,6 +99,11 @@ struct Handle {
   DBuf<double> w1;
   DBuf<int32_t> cptr;         // concatenated child pointers: level k block at cptr_off[k-1]
   std::vector<int64_t> cptr_off;
+  // heavy aggregates (more than HEAVY_AGG children), per parent level k+1:
+  // nested ids heavy[heavy_off[k-1] .. heavy_off[k]) -- a CTA each in the
+  // per-level sweep kernels
+  DBuf<int32_t> heavy;
+  std::vector<int64_t> heavy_off;
   // MSP block-tree factors, packed:
   //   kinv[3 (off_{k+1} - n + B) + {0,1,2}] = K'^{-1} (uu, uv, vv) of aggregate B at level k+1
   //   lof[3 (lo_off[k-1] + p - 2B - 2) + {0,1,2}] = (s w_xu / d, s w_xv / d, 1 / d) of leftover p
@@ -113,7 +120,7 @@ struct Handle {
   // ---- level-1 Laplacian in SELL-32 (slices of 32 rows, column-major,
   // padded with (self, 0)); rows of degree > LCAP are "long": empty in SELL,
   // flagged in sell_mask and handled warp-per-row from the nested CSR
-  int64_t nslices = 0, nlong = 0;
+  int64_t nslices = 0, nlong = 0, nhuge = 0;  // long rows: warp per row; huge: CTA per row (after them)
   int sell_maxw = 0;          // widest slice (padded row length)
   bool sell_uniform = false;  // every slice padded to sell_maxw (no slice pointers needed)
   DBuf<int64_t> sell_ptr;

@@ -14,6 +14,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 
@@ -38,6 +40,8 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+constexpr int64_t HEAVY_DEG = 512;  // rows longer than this get a CTA in the matching
+
 // ------------------------------------------------------------------ MWM
 // Sequential rule: visit vertices in random order; an
 // unmatched vertex takes its heaviest unmatched neighbour (ties: lowest index).
@@ -53,7 +57,9 @@ __global__ void k_mwm_propose(int64_t n, const int64_t* __restrict__ rowptr,
                               uint64_t base, unsigned int* __restrict__ nactive) {
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int found = 0;
-  if (v < n) {
+  if (v < n && rowptr[v + 1] - rowptr[v] > HEAVY_DEG) {
+    found = best[v] >= 0;  // a heavy vertex: k_mwm_propose_heavy's (same round, launched before)
+  } else if (v < n) {
     int32_t b = -1;
     if (mate[v] == -1) {
       const uint64_t pv = mix64(base ^ (uint64_t)v);
@@ -81,6 +87,78 @@ __global__ void k_mwm_propose(int64_t n, const int64_t* __restrict__ rowptr,
   }
   unsigned m = __ballot_sync(0xffffffffu, found);
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(nactive, (unsigned)__popc(m));
+}
+
+// The same proposal for a vertex of degree > HEAVY_DEG, a CTA per vertex: each
+// thread scans a strided share of the row, then the strict total order of
+// the keys picks one winner (the result equals the sequential scan's).
+struct MwmKey {
+  int32_t b;
+  uint64_t kp;
+  int64_t kf, ks;
+  double kw;
+};
+
+__device__ __forceinline__ bool mwm_better(const MwmKey& a, const MwmKey& c) {  // a better than c
+  if (a.b < 0) return false;
+  if (c.b < 0) return true;
+  return a.kp < c.kp ||
+         (a.kp == c.kp && (a.kf < c.kf || (a.kf == c.kf && (a.kw > c.kw || (a.kw == c.kw && a.ks < c.ks)))));
+}
+
+__device__ __forceinline__ MwmKey mwm_shfl(const MwmKey& k, int o) {
+  MwmKey r;
+  r.b = __shfl_xor_sync(0xffffffffu, k.b, o);
+  r.kp = __shfl_xor_sync(0xffffffffu, k.kp, o);
+  r.kf = __shfl_xor_sync(0xffffffffu, k.kf, o);
+  r.ks = __shfl_xor_sync(0xffffffffu, k.ks, o);
+  r.kw = __shfl_xor_sync(0xffffffffu, k.kw, o);
+  return r;
+}
+
+constexpr int HEAVY_TPB = 256;
+
+__global__ void __launch_bounds__(HEAVY_TPB) k_mwm_propose_heavy(const int32_t* __restrict__ heavy,
+                                                                 const int64_t* __restrict__ rowptr,
+                                                                 const int32_t* __restrict__ col,
+                                                                 const double* __restrict__ w,
+                                                                 int32_t* __restrict__ mate,
+                                                                 int32_t* __restrict__ best, uint64_t base) {
+  const int64_t v = heavy[blockIdx.x];
+  __shared__ MwmKey sk[HEAVY_TPB / 32];
+  if (mate[v] != -1) {  // matched or a known leftover: no proposal (as the thread kernel)
+    if (threadIdx.x == 0) best[v] = -1;
+    return;
+  }
+  const uint64_t pv = mix64(base ^ (uint64_t)v);
+  MwmKey k{-1, 0, 0, 0, 0.0};
+  for (int64_t e = rowptr[v] + threadIdx.x; e < rowptr[v + 1]; e += HEAVY_TPB) {
+    const int32_t u = col[e];
+    if (u == v || mate[u] >= 0) continue;
+    const uint64_t pu = mix64(base ^ (uint64_t)u);
+    const bool vfirst = (pv < pu) || (pv == pu && v < u);
+    MwmKey c{u, vfirst ? pv : pu, vfirst ? v : (int64_t)u, vfirst ? (int64_t)u : v, w[e]};
+    if (mwm_better(c, k)) k = c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const MwmKey c = mwm_shfl(k, o);
+    if (mwm_better(c, k)) k = c;
+  }
+  if ((threadIdx.x & 31) == 0) sk[threadIdx.x >> 5] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    MwmKey t = sk[0];
+    for (int i = 1; i < HEAVY_TPB / 32; ++i)
+      if (mwm_better(sk[i], t)) t = sk[i];
+    if (t.b < 0) mate[v] = -2;
+    best[v] = t.b;
+  }
+}
+
+__global__ void k_flag_deg(int64_t n, const int64_t* __restrict__ rowptr, int64_t dmin, int32_t* __restrict__ f) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < n) f[v] = (rowptr[v + 1] - rowptr[v] > dmin) ? 1 : 0;
 }
 
 __global__ void k_mwm_match(int64_t n, const int32_t* __restrict__ best, int32_t* __restrict__ mate) {
@@ -355,7 +433,9 @@ __global__ void k_fill_uniform_ptr(int64_t ns, int64_t stride, int64_t* __restri
   if (s <= ns) sptr[s] = s * stride;
 }
 
-__global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restrict__ rowptr, int lcap,
+// islong: 1 for a long row (warp per row in the SpMV), 2 for a huge one
+// (degree > hcap: a CTA per row)
+__global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restrict__ rowptr, int lcap, int hcap,
                              int64_t* __restrict__ width, uint32_t* __restrict__ mask, int32_t* __restrict__ islong,
                              int* __restrict__ maxw) {
   const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -365,12 +445,30 @@ __global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restri
   int deg = 0;
   if (r < n) deg = rowptr[r + 1] - rowptr[r];
   const bool lng = deg > lcap;
-  if (r < n) islong[r] = lng ? 1 : 0;
+  if (r < n) islong[r] = lng ? (deg > hcap ? 2 : 1) : 0;
   int w = lng ? 0 : deg;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
   const uint32_t m = __ballot_sync(0xffffffffu, lng);
   if (lane == 0) { width[s] = 32 * (int64_t)w; mask[s] = m; atomicMax(maxw, w); }
+}
+
+__global__ void k_flag_heavy(int64_t nB, const int32_t* __restrict__ cptr, int32_t* __restrict__ f) {
+  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (B < nB) f[B] = (cptr[B + 1] - cptr[B] > HEAVY_AGG) ? 1 : 0;
+}
+
+__global__ void k_max_degree(int64_t n, const int32_t* __restrict__ rowptr, int* __restrict__ md) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int d = (i < n) ? rowptr[i + 1] - rowptr[i] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if ((threadIdx.x & 31) == 0 && d > 0) atomicMax(md, d);
+}
+
+__global__ void k_flag_eq(int64_t n, const int32_t* __restrict__ v, int32_t want, int32_t* __restrict__ f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) f[i] = (v[i] == want) ? 1 : 0;
 }
 
 __global__ void k_sell_fill(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
@@ -569,9 +667,25 @@ void validate_csr(Handle& h, const int64_t* rowptr, const int32_t* col, const do
 }
 
 // ------------------------------------------------------------------ driver
+// MSP_SETUP_TIMING=1: per-phase setup times on stderr (synchronises the stream)
+struct SetupClock {
+  bool on = std::getenv("MSP_SETUP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t st, const char* what, int k = -1) {
+    if (!on) return;
+    MSP_CUDA(cudaStreamSynchronize(st));
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+    if (k >= 0) std::fprintf(stderr, "[setup] %-22s level %2d %9.2f ms\n", what, k, ms);
+    else std::fprintf(stderr, "[setup] %-31s %9.2f ms\n", what, ms);
+    t = now;
+  }
+};
+
 void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const double* w_d,
                  cudaStream_t st) {
   Temp tmp;
+  SetupClock clk;
   cudaEvent_t e0, e1;
   MSP_CUDA(cudaEventCreate(&e0));
   MSP_CUDA(cudaEventCreate(&e1));
@@ -609,16 +723,33 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     best.alloc(nk);
     MSP_CUDA(cudaMemsetAsync(mate.p, 0xff, nk * sizeof(int32_t), st));  // -1
     const uint64_t base = mix64(h.seed + 0x9E3779B97F4A7C15ULL * (uint64_t)(k + 1));
-    for (;;) {
-      MSP_CUDA(cudaMemsetAsync(cnt_d.p, 0, sizeof(unsigned), st));
-      k_mwm_propose<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, ww, mate.p, best.p, base, cnt_d.p);
-      MSP_LAUNCH_CHECK();
-      const unsigned active = d2h_scalar(cnt_d.p, st);
-      ++h.mwm_rounds;
-      if (active == 0) break;
-      k_mwm_match<<<grid_for(nk), TPB, 0, st>>>(nk, best.p, mate.p);
-      MSP_LAUNCH_CHECK();
+    // heavy vertices of this level (a CTA each in the proposal)
+    DBuf<int32_t> hv;
+    int64_t nhv = 0;
+    {
+      DBuf<int32_t> ids, fl, nsel;
+      ids.alloc(nk); fl.alloc(nk); nsel.alloc(1); hv.alloc(nk);
+      k_iota32<<<grid_for(nk), TPB, 0, st>>>(nk, ids.p);
+      k_flag_deg<<<grid_for(nk), TPB, 0, st>>>(nk, rp, HEAVY_DEG, fl.p);
+      size_t bytes = 0;
+      MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, fl.p, hv.p, nsel.p, nk, st));
+      MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, hv.p, nsel.p, nk, st));
+      nhv = d2h_scalar(nsel.p, st);
     }
+    // rounds run in batches between host checks: a round after the last
+    // productive one proposes nothing and matches nothing
+    for (int batch = 1;; batch = std::min(batch * 2, 32)) {
+      for (int i = 0; i < batch; ++i) {
+        MSP_CUDA(cudaMemsetAsync(cnt_d.p, 0, sizeof(unsigned), st));
+        if (nhv) k_mwm_propose_heavy<<<(unsigned)nhv, HEAVY_TPB, 0, st>>>(hv.p, rp, cl, ww, mate.p, best.p, base);
+        k_mwm_propose<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, ww, mate.p, best.p, base, cnt_d.p);
+        k_mwm_match<<<grid_for(nk), TPB, 0, st>>>(nk, best.p, mate.p);
+      }
+      MSP_LAUNCH_CHECK();
+      h.mwm_rounds += batch;
+      if (d2h_scalar(cnt_d.p, st) == 0) break;
+    }
+    clk.mark(st, "matching", k);
     // numbering
     flag.alloc(nk);
     scan.alloc(nk);
@@ -635,6 +766,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     k_leftover<<<grid_for(nk), TPB, 0, st>>>(nk, rp, cl, ww, mate.p, agg.p, err_d.p);
     MSP_LAUNCH_CHECK();
     if (d2h_scalar(err_d.p, st)) throw Error{MSP_ERR_GRAPH, "isolated vertex: graph not connected"};
+    clk.mark(st, "leftovers", k);
 
     // ---- coarse graph (Galerkin weights, reading R4 summation order)
     DBuf<int64_t> cnt, pos;
@@ -675,6 +807,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     h.canon_col.push_back(std::move(ccol));
     h.canon_w.push_back(std::move(cw));
     h.lv.push_back(LevelHost{nc, nruns, 0});
+    clk.mark(st, "coarse graph", k);
   }
   h.levels = (int32_t)h.lv.size();
   const int L = h.levels;
@@ -724,6 +857,38 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     MSP_LAUNCH_CHECK();
   }
 
+  // heavy aggregates per parent level
+  {
+    h.heavy_off.assign(L, 0);
+    int64_t maxB = 1;
+    for (int k = 1; k < L; ++k) maxB = std::max<int64_t>(maxB, h.lv[k].n);
+    DBuf<int32_t> ids, fl, sel, nsel;
+    ids.alloc(maxB); fl.alloc(maxB); sel.alloc(maxB); nsel.alloc(1);
+    k_iota32<<<grid_for(maxB), TPB, 0, st>>>(maxB, ids.p);
+    std::vector<std::vector<int32_t>> lists(L);
+    int64_t tot = 0;
+    for (int k = 1; k < L; ++k) {
+      const int64_t nB = h.lv[k].n;
+      k_flag_heavy<<<grid_for(nB), TPB, 0, st>>>(nB, h.cptr.p + h.cptr_off[k - 1], fl.p);
+      size_t bytes = 0;
+      MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, fl.p, sel.p, nsel.p, nB, st));
+      MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, sel.p, nsel.p, nB, st));
+      const int64_t c = d2h_scalar(nsel.p, st);
+      lists[k - 1].resize(c);
+      if (c) MSP_CUDA(cudaMemcpyAsync(lists[k - 1].data(), sel.p, c * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+      h.heavy_off[k - 1] = tot;
+      tot += c;
+    }
+    h.heavy_off[L - 1] = tot;
+    h.heavy.alloc(std::max<int64_t>(tot, 1));
+    for (int k = 1; k < L; ++k)
+      if (!lists[k - 1].empty())
+        MSP_CUDA(cudaMemcpyAsync(h.heavy.p + h.heavy_off[k - 1], lists[k - 1].data(),
+                                 lists[k - 1].size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    MSP_CUDA(cudaStreamSynchronize(st));
+  }
+  clk.mark(st, "nested numbering");
   // ---- level-1 adjacency in nested numbering
   if (h.nnz_adj >= (int64_t)INT32_MAX) throw Error{MSP_ERR_UNSUPPORTED, "nnz >= 2^31"};
   h.perm.alloc(n);
@@ -743,6 +908,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     MSP_LAUNCH_CHECK();
   }
 
+  clk.mark(st, "nested adjacency");
   // ---- MSP block-tree factors, bottom-up
   const int64_t nt = h.n_tilde;
   h.lo_off.assign(L, 0);
@@ -781,6 +947,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     GN += reduce_sum(tmp, gpart.p, nk1, st);
   }
   h.GN = GN;
+  clk.mark(st, "factors");
 
   // ---- gdot weights H = G_1 (top-down over the hierarchy)
   {
@@ -801,9 +968,22 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     MSP_CUDA(cudaStreamSynchronize(st));
   }
 
+  clk.mark(st, "gdot weights");
   // ---- level-1 Laplacian in SELL-32 for the solve
   {
+    // rows above lcap go to the warp-per-row path: 64 by default; 16 for a
+    // heavy-tailed degree distribution (max degree > 64 x mean), whose few
+    // long rows would otherwise pad most slices
     int lcap = 64;
+    {
+      DBuf<int> md;
+      md.alloc(1);
+      MSP_CUDA(cudaMemsetAsync(md.p, 0, sizeof(int), st));
+      k_max_degree<<<grid_for(n), TPB, 0, st>>>(n, h.rowptr1.p, md.p);
+      MSP_LAUNCH_CHECK();
+      const int maxdeg = d2h_scalar(md.p, st);
+      if ((double)maxdeg > 64.0 * (double)h.nnz_adj / (double)n) lcap = 16;
+    }
     if (const char* e = std::getenv("MSP_SELL_LCAP")) lcap = std::max(1, std::atoi(e));
     const int64_t ns = (n + 31) / 32;
     h.nslices = ns;
@@ -817,8 +997,10 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     DBuf<int> mw;
     mw.alloc(1);
     MSP_CUDA(cudaMemsetAsync(mw.p, 0, sizeof(int), st));
-    k_sell_width<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.rowptr1.p, lcap, width.p, h.sell_mask.p, islong.p,
-                                                    mw.p);
+    int hcap = 2048;
+    if (const char* e = std::getenv("MSP_SELL_HUGE")) hcap = std::max(lcap, std::atoi(e));
+    k_sell_width<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.rowptr1.p, lcap, hcap, width.p, h.sell_mask.p,
+                                                    islong.p, mw.p);
     h.sell_maxw = d2h_scalar(mw.p, st);
     MSP_LAUNCH_CHECK();
     exclusive_scan(tmp, width.p, h.sell_ptr.p, ns + 1, st);
@@ -843,12 +1025,19 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     nsel.alloc(1);
     k_iota32<<<grid_for(n), TPB, 0, st>>>(n, ids.p);
     h.long_rows.alloc(n);
+    DBuf<int32_t> fl;
+    fl.alloc(n);
     size_t bytes = 0;
-    MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, islong.p, h.long_rows.p, nsel.p, n, st));
-    MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, islong.p, h.long_rows.p, nsel.p, n, st));
+    MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, fl.p, h.long_rows.p, nsel.p, n, st));
+    k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 1, fl.p);
+    MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p, nsel.p, n, st));
     h.nlong = d2h_scalar(nsel.p, st);
+    k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 2, fl.p);  // huge rows follow the long ones
+    MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p + h.nlong, nsel.p, n, st));
+    h.nhuge = d2h_scalar(nsel.p, st);
   }
 
+  clk.mark(st, "SELL");
   // ---- top level: dense pseudo-inverse of sigma_l L_l
   {
     DBuf<double> M, A;
@@ -866,7 +1055,9 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     MSP_CUDA(cudaStreamSynchronize(st));
   }
 
+  clk.mark(st, "top pseudo-inverse");
   build_schedule(h, st);
+  clk.mark(st, "schedule");
   MSP_CUDA(cudaEventRecord(e1, st));
   MSP_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;

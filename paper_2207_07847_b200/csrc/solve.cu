@@ -306,6 +306,26 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
   }
 }
 
+// sum_e w_e (pi - p(col_e)) over e = e0 + sub, e0 + sub + S, ... < e1 with
+// four independent chains (the column and gather loads of four entries are
+// in flight together: long rows are latency bound otherwise)
+template <int S, typename PJ>
+__device__ __forceinline__ double row_dot(const int32_t* __restrict__ col, const double* __restrict__ w, int32_t e0,
+                                          int32_t e1, int sub, double pi, PJ pj) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int32_t e = e0 + sub;
+  for (; e + 3 * S < e1; e += 4 * S) {
+    const int32_t j0 = col[e], j1 = col[e + S], j2 = col[e + 2 * S], j3 = col[e + 3 * S];
+    const double w0 = w[e], w1 = w[e + S], w2 = w[e + 2 * S], w3 = w[e + 3 * S];
+    a0 += w0 * (pi - pj(j0));
+    a1 += w1 * (pi - pj(j1));
+    a2 += w2 * (pi - pj(j2));
+    a3 += w3 * (pi - pj(j3));
+  }
+  for (; e < e1; e += S) a0 += w[e] * (pi - pj(col[e]));
+  return (a0 + a1) + (a2 + a3);
+}
+
 // PCG scalars after the level-1 output: rz = (r, R r)
 __device__ __forceinline__ void finish_rz(double rz, double* scal, int mode) {
   if (mode == M_ITER) scal[S_BETA] = rz / scal[S_RHO];
@@ -348,7 +368,7 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ perm, const dou
 template <bool PCG>
 __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                               const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                              const uint32_t* __restrict__ smask, int64_t nlong,
+                                              const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
                                               const int32_t* __restrict__ long_rows,
                                               const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                               const double* __restrict__ w, const double* __restrict__ z,
@@ -398,14 +418,27 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
     if (r < row0 || r >= row1) continue;
     const double po = PCG ? pold[r] : 0.0;
     const double pi = PCG ? z[r] + beta * po : z[r];
-    double acc = 0.0;
-    for (int32_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
-      const int32_t j = col[e];
-      const double pj = PCG ? z[j] + beta * pold[j] : z[j];
-      acc += w[e] * (pi - pj);
-    }
+    double acc = row_dot<32>(col, w, rowptr[r], rowptr[r + 1], lane, pi,
+                             [&](int32_t j) { return PCG ? z[j] + beta * pold[j] : z[j]; });
     acc = warp_sum(acc);
     if (lane == 0) {
+      q[r] = acc;
+      if (PCG) {
+        pnew[r] = pi;
+        x[r] += alpha * po;
+        d += pi * acc;
+      }
+    }
+  }
+  for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
+    const int64_t r = long_rows[nlong + i];
+    if (r < row0 || r >= row1) continue;  // block-uniform
+    const double po = PCG ? pold[r] : 0.0;
+    const double pi = PCG ? z[r] + beta * po : z[r];
+    double acc = row_dot<TPB>(col, w, rowptr[r], rowptr[r + 1], threadIdx.x, pi,
+                              [&](int32_t j) { return PCG ? z[j] + beta * pold[j] : z[j]; });
+    acc = block_sum<TPB>(acc);
+    if (threadIdx.x == 0) {
       q[r] = acc;
       if (PCG) {
         pnew[r] = pi;
@@ -439,7 +472,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 template <int MW, bool UNIF>
 __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                                      const uint32_t* __restrict__ smask, int64_t nlong,
+                                                      const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
                                                       const int32_t* __restrict__ long_rows,
                                                       const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                       const double* __restrict__ w, const double2* __restrict__ zp,
@@ -548,16 +581,32 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices
     const double2 vr = zp[r];
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
-    double acc = 0.0;
-    for (int32_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
-      const double2 v = zp[col[e]];
-      acc += w[e] * (pi - (v.x + beta * v.y));
-    }
+    double acc = row_dot<32>(col, w, rowptr[r], rowptr[r + 1], lane, pi, [&](int32_t j) {
+      const double2 v = zp[j];
+      return v.x + beta * v.y;
+    });
     acc = warp_sum(acc);
     if (lane == 0) {
       q[r] = acc;
       zpout[2 * r + 1] = pi;
       x[r] += alpha * pr;
+      d += pi * acc;
+    }
+  }
+  for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
+    const int64_t row = long_rows[nlong + i];
+    const double2 vr = zp[row];
+    const double pr = vr.y;
+    const double pi = vr.x + beta * pr;
+    double acc = row_dot<TPB>(col, w, rowptr[row], rowptr[row + 1], threadIdx.x, pi, [&](int32_t j) {
+      const double2 v = zp[j];
+      return v.x + beta * v.y;
+    });
+    acc = block_sum<TPB>(acc);
+    if (threadIdx.x == 0) {
+      q[row] = acc;
+      zpout[2 * row + 1] = pi;
+      x[row] += alpha * pr;
       d += pi * acc;
     }
   }
@@ -812,7 +861,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 template <int MW, bool UNIF>
 __global__ void __launch_bounds__(TPB, 4) k_spmv_up(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                                    const uint32_t* __restrict__ smask, int64_t nlong,
+                                                    const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
                                                     const int32_t* __restrict__ long_rows,
                                                     const int32_t* __restrict__ rowptr,
                                                     const int32_t* __restrict__ col, const double* __restrict__ w,
@@ -927,13 +976,29 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_up(int64_t n, int64_t nslices, 
       const double2 vr = zp[row];
       const double pr = vr.y;
       const double pi = vr.x + beta * pr;
-      double acc = 0.0;
-      for (int32_t e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
-        const double2 v = zp[col[e]];
-        acc += w[e] * (pi - (v.x + beta * v.y));
-      }
+      double acc = row_dot<32>(col, w, rowptr[row], rowptr[row + 1], lane, pi, [&](int32_t j) {
+        const double2 v = zp[j];
+        return v.x + beta * v.y;
+      });
       acc = warp_sum(acc);
       if (lane == 0) {
+        q[row] = acc;
+        zpout[2 * row + 1] = pi;
+        x[row] += alpha_old * pr;
+        d += pi * acc;
+      }
+    }
+    for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
+      const int64_t row = long_rows[nlong + i];
+      const double2 vr = zp[row];
+      const double pr = vr.y;
+      const double pi = vr.x + beta * pr;
+      double acc = row_dot<TPB>(col, w, rowptr[row], rowptr[row + 1], threadIdx.x, pi, [&](int32_t j) {
+        const double2 v = zp[j];
+        return v.x + beta * v.y;
+      });
+      acc = block_sum<TPB>(acc);
+      if (threadIdx.x == 0) {
         q[row] = acc;
         zpout[2 * row + 1] = pi;
         x[row] += alpha_old * pr;
@@ -1306,16 +1371,32 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
 // aggregate)  y_{k+1} = P^T y_k
 __global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
                                                 const double* __restrict__ yin, double* __restrict__ yout,
-                                                const unsigned int* __restrict__ cnt, int mode_in) {
+                                                const unsigned int* __restrict__ cnt, int mode_in,
+                                                const int32_t* __restrict__ heavy, int nheavy) {
+  // blocks [0, G - nheavy): a thread per aggregate (heavy ones skipped);
+  // blocks [G - nheavy, G): a CTA per heavy aggregate
   const int mode = mode_in & 15;
   pdl_wait();
   if (mode == M_ITER && cnt[C_DONE]) return;
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (B < lv.n[k]) {
-    const int32_t* cp = cptr + lv.cpo[k - 1];
+  const int32_t* cp = cptr + lv.cpo[k - 1];
+  const int nnorm = (int)gridDim.x - nheavy;
+  if ((int)blockIdx.x < nnorm) {
+    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < lv.n[k]) {
+      const int32_t c0 = cp[B], c1 = cp[B + 1];
+      if (c1 - c0 <= HEAVY_AGG) {
+        double y = 0.0;
+#pragma unroll 1
+        for (int32_t c = c0; c < c1; ++c) y += yin[c];
+        yout[B] = y;
+      }
+    }
+  } else {
+    const int64_t B = heavy[blockIdx.x - nnorm];
     double y = 0.0;
-    for (int32_t c = cp[B]; c < cp[B + 1]; ++c) y += yin[c];
-    yout[B] = y;
+    for (int32_t c = cp[B] + threadIdx.x; c < cp[B + 1]; c += TPB) y += yin[c];
+    y = block_sum<TPB>(y);
+    if (threadIdx.x == 0) yout[B] = y;
   }
 }
 
@@ -1327,27 +1408,57 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
                                                   const double* __restrict__ zB, const double* __restrict__ wB,
                                                   double* __restrict__ zk, double* __restrict__ wk,
                                                   double* __restrict__ part, double* __restrict__ scal,
-                                                  unsigned int* __restrict__ cnt, int mode_in) {
+                                                  unsigned int* __restrict__ cnt, int mode_in,
+                                                  const int32_t* __restrict__ heavy, int nheavy) {
   const int mode = mode_in & 15;
   const int zs = (mode_in & M_ZS2) ? 2 : 1;
   pdl_wait();
   if (mode != M_APPLY && cnt[C_DONE]) return;
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const double rho = scal[S_SHIFT];
   const double ckk = lv.ck[k];
+  const int32_t* cp = cptr + lv.cpo[k - 1];
+  const double* Nk = Nsub + lv.off[k - 1];
+  auto tf = [&](int64_t p) { return LEVEL1 ? yk[p] - rho : ckk * yk[p] - rho * Nk[p]; };
   double rz = 0.0;
-  if (B < lv.n[k]) {
-    const int32_t* cp = cptr + lv.cpo[k - 1];
-    const double* Nk = Nsub + lv.off[k - 1];
+  auto ef = [&](int64_t p, double z, double w) {
+    if (LEVEL1) { rz += yk[p] * w; wk[zs * p] = w; }
+    else { zk[p] = z; wk[p] = w; }
+  };
+  const int nnorm = (int)gridDim.x - nheavy;
+  if ((int)blockIdx.x < nnorm) {
+    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < lv.n[k] && cp[B + 1] - cp[B] <= HEAVY_AGG) {
+      const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
+      const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
+      block_solve(
+          cp[B], cp[B + 1], [&](int j) { return ki[j]; }, [&](int64_t p, int j) { return lof[lb + 3 * p + j]; },
+          zB[B], lv.negmu * wB[B], tf, ef);
+    }
+  } else {  // a CTA per heavy aggregate: the leftover sums by a block reduction
+    const int64_t B = heavy[blockIdx.x - nnorm];
+    const int64_t s0 = cp[B], s1 = cp[B + 1];
     const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
     const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
-    block_solve(
-        cp[B], cp[B + 1], [&](int j) { return ki[j]; }, [&](int64_t p, int j) { return lof[lb + 3 * p + j]; }, zB[B],
-        lv.negmu * wB[B], [&](int64_t p) { return LEVEL1 ? yk[p] - rho : ckk * yk[p] - rho * Nk[p]; },
-        [&](int64_t p, double z, double w) {
-          if (LEVEL1) { rz += yk[p] * w; wk[zs * p] = w; }
-          else { zk[p] = z; wk[p] = w; }
-        });
+    const double kuu = ki[0], kuv = ki[1], kvv = ki[2];
+    const double zb = zB[B], wbm = lv.negmu * wB[B];
+    double su = 0.0, sv = 0.0;
+    for (int64_t p = s0 + 2 + threadIdx.x; p < s1; p += TPB) {
+      const double tx = tf(p);
+      su += lof[lb + 3 * p + 0] * tx;
+      sv += lof[lb + 3 * p + 1] * tx;
+    }
+    const double2 s2 = block_sum2<TPB>(make_double2(su, sv));
+    const double au = tf(s0) + s2.x, av = tf(s0 + 1) + s2.y;
+    const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
+    if (threadIdx.x == 0) {
+      { const double z = zb + zu; ef(s0, z, z + wbm); }
+      { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
+    }
+    for (int64_t p = s0 + 2 + threadIdx.x; p < s1; p += TPB) {
+      const double zx = lof[lb + 3 * p + 2] * tf(p) + lof[lb + 3 * p + 0] * zu + lof[lb + 3 * p + 1] * zv;
+      const double z = zb + zx;
+      ef(p, z, z + wbm);
+    }
   }
   if (LEVEL1) {
     rz = block_sum<TPB>(rz);
@@ -2004,8 +2115,9 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     if (T.generic) {
       const int k = T.k0;
       const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
-      launch(k_up_lvl, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin, h.Y.p + h.lv[k].off,
-             (const unsigned*)cnt, mode);
+      const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
+      launch(k_up_lvl, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin,
+             h.Y.p + h.lv[k].off, (const unsigned*)cnt, mode, (const int32_t*)(h.heavy.p + h.heavy_off[k - 1]), nh);
       P.end(PC_MID_UP);
     } else {
       if (T.k0 == 1)
@@ -2040,16 +2152,18 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     if (T.generic) {
       const int k = T.k0;
       const int64_t ok = h.lv[k - 1].off, op = h.lv[k].off;
+      const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
+      const int32_t* hv = h.heavy.p + h.heavy_off[k - 1];
       if (k == 1)
-        launch(k_down_lvl<true>, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+        launch(k_down_lvl<true>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
                (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p,
                (const double*)(h.Z.p + op), (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt,
-               mode);
+               mode, hv, nh);
       else
-        launch(k_down_lvl<false>, grid_for(h.lv[k].n), TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+        launch(k_down_lvl<false>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
                (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)(h.Y.p + ok),
                (const double*)h.Nsub.p, (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok,
-               h.W.p + ok, part_rz, scal, cnt, mode);
+               h.W.p + ok, part_rz, scal, cnt, mode, hv, nh);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1)
@@ -2075,7 +2189,7 @@ template <bool PCG>
 void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
                  cudaStream_t st) {
   launch(k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-         (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
+         (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
          (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
          (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, (int64_t)0, h.n);
   ++h.launches;
@@ -2095,7 +2209,7 @@ void launch_spmv_up(Handle& h, const Lv& lv, const double* zp_in, double* zp_out
   auto& T = h.tiers[0];
   auto go = [&](auto kern) {
     launch(kern, h.fuse_grid, TPB, T.smem_up, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
+           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
            (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
            (const double*)h.w1.p, reinterpret_cast<const double2*>(zp_in), zp_out, h.vq.p, x, h.red.p, lv, T.desc,
            (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, h.vr.p, (const double*)h.Hvec.p, h.Y.p,
@@ -2114,7 +2228,7 @@ void launch_spmv_up(Handle& h, const Lv& lv, const double* zp_in, double* zp_out
 void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
   auto go = [&](auto kern) {
     launch(kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
-           (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, (const int32_t*)h.long_rows.p,
+           (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge, (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
   };
@@ -2530,7 +2644,7 @@ void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x
                "alltoallv(p halo)");
     if (nrecv) k_put<<<grid_for(nrecv), TPB, 0, st>>>(nrecv, d.recv_idx.p, d.recvbuf.p, h.vp.p);
     launch(k_spmv<false>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong,
+           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
            (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
            (const double*)h.w1.p, (const double*)h.vp.p, (const double*)nullptr, (double*)nullptr, h.vq.p,
            (double*)nullptr, h.red.p, h.scal.p, h.counters.p, d.row0, d.row1);

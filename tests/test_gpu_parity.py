@@ -56,6 +56,9 @@ GRAPHS = {
     # large enough for tiers + the coarse GEMV (n_Kc <= 512 below a tiled top tier)
     "grid_90x70_loguniform": lambda: G.grid2d(90, 70, "loguniform", 8),
     "rgg_12000": lambda: G.rgg(12000, 12.0, 2),
+    # power law: hub rows > 2048 (a CTA per row in the SpMV), vertices of
+    # degree > 512 (a CTA each in the matching), aggregates of > 64 children
+    "chung_lu_30000": lambda: G.chung_lu(30000, 2.1, 16.0, 7),
 }
 
 
