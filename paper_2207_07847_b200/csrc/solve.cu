@@ -1496,8 +1496,8 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
   const int mode = mode_in & 15;
   const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ double srho;
-  auto W = [&](int t) {
-    const int c = (int)((lv.n[Kc + t - 1] + 31) >> 5);
+  auto W = [&](int t) {  // tb[t].cnt = n_{Kc+t} (shared memory)
+    const int c = (tb[t].cnt + 31) >> 5;
     return c < 1 ? 1 : (c > NW ? NW : c);
   };
   __syncthreads();  // pointer table and staged segments
