@@ -139,6 +139,7 @@ struct Handle {
     bool generic = false;     // one level by per-node kernels (an aggregate too large to tile)
     TierDesc desc{};
     DBuf<int32_t> firstk0;    // [n_k1 + 1]: first level-k0 descendant of each level-k1 node
+    DBuf<int4> segs;          // [ntiles][desc.nseg] static segments of the down kernel (sched.cuh)
     int up_group = 1;         // tiles per CTA of the up kernel
   };
   std::vector<Tier> tiers;

@@ -46,7 +46,15 @@ struct TierDesc {
   // node of the tile (int32, [a, b]) and y at level k0
   int o_uf, o_uy0, o_uq, o_uh, smem_up;
   int up_group;    // tiles per CTA of the up kernel (1 when distributed)
+  int nseg;        // static (constant-data) segments per tile of the down kernel
 };
+
+// One static TMA segment of a tile of the down kernel, precomputed at setup
+// (the window stage_window would compute): x = kind | t << 2 | dst << 8
+// (kind 0 child pointers, 1 factors, 2 leftover coefficients, 3 N_k0; t the
+// tier level; dst the shared-memory byte offset), y = bytes (0: nothing to
+// copy), z = first element of the 16-byte aligned window, w = skew.
+enum { SEG_CP = 0, SEG_KI = 1, SEG_LO = 2, SEG_N0 = 3 };
 
 // coarse kernel (levels Kc..L, one CTA), t = level Kc+t; same conventions,
 // every range is a whole level

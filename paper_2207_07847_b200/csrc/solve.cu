@@ -1114,7 +1114,8 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
                                                   double* __restrict__ zout, double* __restrict__ part,
                                                   double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode_in,
                                                   const double* __restrict__ Mco, const double* __restrict__ part_gd,
-                                                  int npart_gd, const double* __restrict__ Ygl, int tile0) {
+                                                  int npart_gd, const double* __restrict__ Ygl, int tile0,
+                                                  const int4* __restrict__ segs) {
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
@@ -1134,30 +1135,29 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     sa[tid] = a;
     sn[tid] = tstart[tid * nt1 + tile + 1] - a;
   }
+  // static segments (child pointers, factors, leftover coefficients, N_k0),
+  // one per thread from the tile's precomputed descriptors; after the grid
+  // dependency: y_k0, z, w
+  int4 sd = make_int4(0, 0, 0, 0);
+  if (tid < td.nseg) sd = __ldg(segs + (int64_t)tile * td.nseg + tid);
   __syncthreads();
-  // segments, one per thread, spread over the warps (g = lane * 8 + warp):
-  // [0, nl-1) child pointers, [nl-1, 2nl-2) factors, [2nl-2, 3nl-3) leftover
-  // coefficients, 3nl-3 N_k0; after the grid dependency: y_k0, z, w
-  const int g = (tid & 31) * (TT / 32) + (tid >> 5);
-  const int m1 = nl - 1;
-  if (g < m1) {
-    const int t = g + 1;
-    const int64_t base = lv.cpo[k0 + t - 2];
-    skc[t] = stage_window<true>(&bar, sm + td.o_cp[t], cptr, 4, base + sa[t], base + sa[t] + sn[t] + 1);
-  } else if (g < 2 * m1) {
-    const int t = g - m1 + 1;
-    const int64_t base = 3 * (lv.off[k0 + t - 1] - n1 + sa[t]);
-    skk[t] = stage_window<true>(&bar, sm + td.o_ki[t], kinv, 8, base, base + 3 * (int64_t)sn[t]);
-  } else if (g < 3 * m1) {
-    const int t = g - 2 * m1;
-    const int64_t lo0 = (int64_t)sa[t] - 2 * (int64_t)sa[t + 1];
-    const int64_t lo1 = (int64_t)(sa[t] + sn[t]) - 2 * (int64_t)(sa[t + 1] + sn[t + 1]);
-    const int64_t base = 3 * lv.lo[k0 + t - 1];
-    skl[t] = stage_window<true>(&bar, sm + td.o_lo[t], lof, 8, base + 3 * lo0, base + 3 * lo1);
-  } else if (!FIRST && g == 3 * m1) {
-    const int64_t base = lv.off[k0 - 1];
-    skn0 = stage_window<true>(&bar, sm + td.o_n[0], Nsub, 8, base + sa[0], base + sa[0] + sn[0]);
+  if (tid < td.nseg) {
+    const int kind = sd.x & 3, t = (sd.x >> 2) & 63, dst = sd.x >> 8;
+    if (sd.y > 0) {
+      mbar_expect_tx(&bar, (uint32_t)sd.y);
+      const char* src = (kind == SEG_CP)   ? (const char*)cptr + (int64_t)sd.z * 4
+                        : (kind == SEG_KI) ? (const char*)kinv + (int64_t)sd.z * 8
+                        : (kind == SEG_LO) ? (const char*)lof + (int64_t)sd.z * 8
+                                           : (const char*)Nsub + (int64_t)sd.z * 8;
+      tma_1d_keep(sm + dst, src, (uint32_t)sd.y, &bar);
+    }
+    if (kind == SEG_CP) skc[t] = sd.w;
+    else if (kind == SEG_KI) skk[t] = sd.w;
+    else if (kind == SEG_LO) skl[t] = sd.w;
+    else skn0 = sd.w;
   }
+  const int g = (tid & 31) * (TT / 32) + (tid >> 5);  // dynamic segments below
+  const int m1 = nl - 1;
   TRACE(1);
   PHASE(0);
   pdl_wait();
@@ -2172,12 +2172,13 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
                cnt, mode | (dc ? M_DIST : 0), (const double*)h.Mco.p, (const double*)part_gd, npart_up,
-               (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0));
+               (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p);
       else
         launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
-               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0);
+               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
+               (const int4*)T.segs.p);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
