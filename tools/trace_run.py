@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 from paper_2207_07847_b200 import build as B  # noqa: E402
 
 lib = os.path.join(ROOT, "build_trace_libmsp.so")
-B.build(force=True, extra=["-DMSP_TRACE"], lib=lib)
+B.build(force=True, extra=["-DMSP_TRACE"] + [f for f in os.environ.get("TRACE_EXTRA", "").split(",") if f], lib=lib)
 code = r"""
 import os, sys, torch
 sys.path.insert(0, %r)
