@@ -152,7 +152,8 @@ struct Handle {
   DBuf<double> Mco;
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
-  unsigned fuse_grid = 0;  // grid of the fused SpMV + first-tier up kernel (0: not used)
+  unsigned fuse_grid = 0;
+  size_t merged_coff = 0, merged_smem = 0;  // merged last-tier down + coarse kernel (0: off)  // grid of the fused SpMV + first-tier up kernel (0: not used)
 
   // ---- PEGP (built lazily on first use, pegp.cu)
   bool pegp_ready = false;

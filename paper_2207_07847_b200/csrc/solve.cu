@@ -1099,14 +1099,259 @@ __global__ void __launch_bounds__(TPB, 4) k_spmv_up(int64_t n, int64_t nslices, 
   TRACE_END();
 }
 
+// --------------------------------------------------------- coarse kernel
+// Levels Kc..L of the coarse kernel when the top has <= 32 nodes.  Level t
+// (n_{Kc+t} nodes, one per thread) runs on its first W(t) = ceil(n/32) warps
+// only; the barrier before a level spans exactly the warps of the larger of
+// the two levels it separates (a named barrier, __syncwarp for one warp), so
+// the small upper levels cost a warp-level sync instead of a 32-warp one.  The
+// top solve runs on warp 0.  Level Kc goes straight to global memory.
+// Barrier ids: 1 for the up sweep (its warp sets only shrink, so every warp
+// of an instance has left the previous one); one id per down level (2 + t),
+// because a warp that joins the down sweep late arrives at its first barrier
+// while the others are still levels above.
+__device__ __forceinline__ void named_sync(int id, int nw) {
+  if (nw == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nw * 32) : "memory");
+}
+
+#undef TRACE_KID
+#define TRACE_KID 1
+__device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, char* sm, const double* __restrict__ pinv,
+                                           double* __restrict__ Zg, double* __restrict__ Wg,
+                                           double* __restrict__ zout, double* __restrict__ scal, double gd,
+                                           int mode_in, int o_tt, bool kc_to_smem = false) {
+  // kc_to_smem: level Kc stays in shared memory (the merged tier-2 down kernel)
+  constexpr int NW = CT / 32;
+  const int mode = mode_in & 15;
+  const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ double srho;
+  auto W = [&](int t) {  // tb[t].cnt = n_{Kc+t} (shared memory)
+    const int c = (tb[t].cnt + 31) >> 5;
+    return c < 1 ? 1 : (c > NW ? NW : c);
+  };
+  __syncthreads();  // pointer table and staged segments
+  // ---- up: level t on warps [0, W(t))
+  for (int t = 1; t < nl; ++t) {
+    if (t >= 2) {
+      const int wp = W(t - 1);
+      if (warp >= wp) break;
+      named_sync(1, wp);
+    }
+    if (t <= 7) TRACE(6 + t);
+    const int wt = W(t);
+    if (warp < wt) {
+      const int* cp = SMP(const int, tb[t].cp);
+      const double* yc = SMP(const double, tb[t - 1].y);
+      double* yp = SMP(double, tb[t].y);
+      const int np = tb[t].cnt;
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        double y = 0.0;
+        const int c1 = cp[i + 1];
+        #pragma unroll 1
+        for (int c = cp[i]; c < c1; ++c) y += yc[c];
+        yp[i] = y;
+      }
+    }
+  }
+  // ---- top solve (warp 0)
+  double rz = 0.0;
+  const int ntop = tb[nl - 1].cnt;
+  if (warp == 0) {
+    __syncwarp();
+    const double* yt = SMP(const double, tb[nl - 1].y);
+    const double* Nt = SMP(const double, tb[nl - 1].nn);
+    double ysum = 0.0;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) ysum += yt[i];
+    ysum = warp_sum(ysum);
+    gd = warp_sum(gd);
+    const double rho = lv.c_sum * ysum / lv.n_tilde;
+    double* tt = reinterpret_cast<double*>(sm + o_tt);
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
+    __syncwarp();
+    double* zt = SMP(double, tb[nl - 1].z);
+    double* wt = SMP(double, tb[nl - 1].w);
+    double nz = 0.0;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) {
+      double zi = 0.0;
+      #pragma unroll 1
+      for (int j = 0; j < ntop; ++j) zi += pinv[i * ntop + j] * tt[j];
+      zt[i] = zi;
+      nz += Nt[i] * zi;
+    }
+    nz = warp_sum(nz);
+    const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
+    #pragma unroll 1
+    for (int i = lane; i < ntop; i += 32) {
+      const double z = zt[i] - m;
+      zt[i] = z;
+      wt[i] = z;
+      if (L == 1) {
+        rz += yt[i] * z;
+        zout[((mode_in & M_ZS2) ? 2 : 1) * i] = z;
+      } else if (nl == 1) {  // the top is level Kc: to global
+        if (mode == M_COLUMN) {
+          Zg[(int64_t)blockIdx.x * 2 * ntop + i] = z;
+          Zg[(int64_t)blockIdx.x * 2 * ntop + ntop + i] = z;
+        } else {
+          Zg[lv.off[Kc - 1] + i] = z;
+          Wg[lv.off[Kc - 1] + i] = z;
+        }
+      }
+    }
+    if (lane == 0) {
+      srho = rho;
+      if (mode != M_COLUMN) scal[S_SHIFT] = rho;
+    }
+    __syncwarp();
+  }
+  TRACE(5);
+  // ---- down: level t on warps [0, W(t)) (W grows as t falls)
+  const double negmu = lv.negmu;
+  for (int t = nl - 2; t >= 0; --t) {
+    const int wt = W(t);
+    if (warp >= wt) continue;
+    named_sync(2 + t, wt);
+    const double rho = srho;
+    const int* cp = SMP(const int, tb[t + 1].cp);
+    const double* ki = SMP(const double, tb[t + 1].ki);
+    const double* zp = SMP(const double, tb[t + 1].z);
+    const double* wp = SMP(const double, tb[t + 1].w);
+    const double* lo = SMP(const double, tb[t].lo);
+    const double* yc = SMP(const double, tb[t].y);
+    const double* nc = SMP(const double, tb[t].nn);
+    double* zc = SMP(double, tb[t].z);
+    double* wc = SMP(double, tb[t].w);
+    const double ckk = tb[t].ck;
+    const int np = tb[t + 1].cnt;
+    const int nk = tb[t].cnt;
+    if (t > 0 || kc_to_smem) {
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zc[p] = z; wc[p] = w; });
+      }
+    } else if (Kc == 1) {  // level-1 output and (r, R r)
+      const int zs = (mode_in & M_ZS2) ? 2 : 1;
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return yc[p] - rho; },
+            [&](int p, double z, double w) { rz += yc[p] * w; zout[zs * p] = w; });
+      }
+    } else {  // level Kc to global: Z, W (or column blockIdx.x of the GEMV map)
+      double* zg = (mode == M_COLUMN) ? Zg + (int64_t)blockIdx.x * 2 * nk : Zg + lv.off[Kc - 1];
+      double* wg = (mode == M_COLUMN) ? zg + nk : Wg + lv.off[Kc - 1];
+      #pragma unroll 1
+      for (int i = tid; i < np; i += 32 * wt) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
+            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zg[p] = z; wg[p] = w; });
+      }
+    }
+  }
+  TRACE(6);
+  pdl_trigger();
+  if (Kc == 1) {
+    rz = block_sum<CT>(rz);
+    if (tid == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
+  }
+}
+
+// Single CTA: levels Kc..L up-sweep, the top solve, levels L..Kc down-sweep,
+// everything staged in / computed into shared memory (layout: CoarseDesc).
+// When Kc == 1 it also produces the level-1 output and (r, R r).
+#undef TRACE_KID
+#define TRACE_KID 1
+// Shared state of the coarse levels (k_coarse, and the merged tier-2 down
+// kernel that runs them first).
+struct CoarseState {
+  uint64_t bar;
+  int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
+  int sky0, skp;
+  LvlPtr tb[MAXT + 8];
+};
+
+// static segments of levels Kc..L (before the grid dependency), one per
+// thread spread over the warps: [0, nl-1) child pointers, [nl-1, 2nl-2)
+// factors, [2nl-2, 3nl-3) leftover coefficients, [3nl-3, 4nl-3) subtree
+// sizes, 4nl-3 the top pseudo-inverse.  C.bar must be initialised and visible.
+template <int NT>
+__device__ __forceinline__ void coarse_stage_static(CoarseState& C, char* smc, const Lv& lv, const CoarseDesc& cd,
+                                                    const int32_t* __restrict__ cptr,
+                                                    const double* __restrict__ kinv,
+                                                    const double* __restrict__ lof,
+                                                    const double* __restrict__ Nsub,
+                                                    const double* __restrict__ pinv_g) {
+  const int tid = threadIdx.x, L = lv.L, Kc = lv.Kc, nl = cd.nl;
+  const int64_t n1 = lv.n[0];
+  const int g = (tid & 31) * (NT / 32) + (tid >> 5);
+  const int m1 = nl - 1;
+  if (g < m1) {
+    const int t = g + 1;
+    const int64_t base = lv.cpo[Kc + t - 2];
+    C.skc[t] = stage_window<true>(&C.bar, smc + cd.o_cp[t], cptr, 4, base, base + lv.n[Kc + t - 1] + 1);
+  } else if (g < 2 * m1) {
+    const int t = g - m1 + 1;
+    const int64_t base = 3 * (lv.off[Kc + t - 1] - n1);
+    C.skk[t] = stage_window<true>(&C.bar, smc + cd.o_ki[t], kinv, 8, base, base + 3 * lv.n[Kc + t - 1]);
+  } else if (g < 3 * m1) {
+    const int t = g - 2 * m1;
+    const int64_t base = 3 * lv.lo[Kc + t - 1];
+    C.skl[t] = stage_window<true>(&C.bar, smc + cd.o_lo[t], lof, 8, base,
+                                  base + 3 * (lv.n[Kc + t - 1] - 2 * lv.n[Kc + t]));
+  } else if (g < 3 * m1 + nl) {
+    const int t = g - 3 * m1;
+    const int64_t base = lv.off[Kc + t - 1];
+    C.skn[t] = stage_window<true>(&C.bar, smc + cd.o_n[t], Nsub, 8, base, base + lv.n[Kc + t - 1]);
+  } else if (g == 3 * m1 + nl && cd.stage_pinv) {
+    const int64_t nt = lv.n[L - 1];
+    C.skp = stage_window<true>(&C.bar, smc + cd.o_pinv, pinv_g, 8, 0, nt * nt);
+  }
+}
+
+// per-level pointer table of the coarse levels (threads t < nl)
+__device__ __forceinline__ void coarse_table(CoarseState& C, const Lv& lv, const CoarseDesc& cd, int coff) {
+  const int t = threadIdx.x, nl = cd.nl, Kc = lv.Kc;
+  if (t < nl) {
+    LvlPtr e;
+    e.cp = (t >= 1) ? coff + cd.o_cp[t] + 4 * C.skc[t] : -1;
+    e.ki = (t >= 1) ? coff + cd.o_ki[t] + 8 * C.skk[t] : -1;
+    e.lo = (t + 1 < nl) ? coff + cd.o_lo[t] + 8 * C.skl[t] : -1;
+    e.y = coff + cd.o_y[t] + (t == 0 ? 8 * C.sky0 : 0);
+    e.nn = coff + cd.o_n[t] + 8 * C.skn[t];
+    e.z = coff + cd.o_z[t];
+    e.w = coff + cd.o_w[t];
+    e.a = 0;
+    e.cnt = (int)lv.n[Kc + t - 1];
+    e.ck = lv.ck[Kc + t];
+    C.tb[t] = e;
+  }
+}
+
 // ---------------------------------------------------------- tile down-sweep
 // Tier k0..k1: recompute y (and subtree sizes N) of levels k0+1..k1-1 from
 // y_k0, read z, w at level k1, solve / prolong down to level k0.  FIRST: the
 // output R r and the partial (r, R r); otherwise z, w at level k0 to global.
 #undef TRACE_KID
 #define TRACE_KID (FIRST ? 2 : 3)
-template <bool FIRST>
-__global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
+// COARSE (tier 2 = the last tier, one CTA of CT threads per tile): the CTA
+// first runs the coarse levels Kc..L itself (every CTA the same, into its own
+// shared memory at byte offset coff) and takes its tile's level-Kc z, w from
+// there -- no coarse kernel, no round trip of z_Kc, w_Kc through global memory.
+template <bool FIRST, bool COARSE = false>
+__global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
                                                   const int32_t* __restrict__ tstart, const int32_t* __restrict__ cptr,
                                                   const double* __restrict__ kinv, const double* __restrict__ lof,
                                                   const double* __restrict__ Nsub, const double* __restrict__ y0src,
@@ -1115,7 +1360,10 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
                                                   double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode_in,
                                                   const double* __restrict__ Mco, const double* __restrict__ part_gd,
                                                   int npart_gd, const double* __restrict__ Ygl, int tile0,
-                                                  const int4* __restrict__ segs) {
+                                                  const int4* __restrict__ segs,
+                                                  const __grid_constant__ CoarseDesc cd, int coff,
+                                                  const double* __restrict__ pinv_g) {
+  constexpr int NT = COARSE ? CT : TT;
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
@@ -1124,12 +1372,17 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   __shared__ int sky0, skn0, skz, skw, sdone;
   __shared__ double srho, srho_g;
   __shared__ LvlPtr tb[MAXT];
+  __shared__ CoarseState C;
+  __shared__ double sgd;
   const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   TRACE(0);
   PHASE_START();
-  if (tid == 0) mbar_init(&bar, 1);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    if (COARSE) mbar_init(&C.bar, 1);
+  }
   if (tid < nl) {
     const int a = tstart[tid * nt1 + tile];
     sa[tid] = a;
@@ -1156,8 +1409,9 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     else if (kind == SEG_LO) skl[t] = sd.w;
     else skn0 = sd.w;
   }
-  const int g = (tid & 31) * (TT / 32) + (tid >> 5);  // dynamic segments below
+  const int g = (tid & 31) * (NT / 32) + (tid >> 5);  // dynamic segments below
   const int m1 = nl - 1;
+  if (COARSE) coarse_stage_static<NT>(C, sm + coff, lv, cd, cptr, kinv, lof, Nsub, pinv_g);
   TRACE(1);
   PHASE(0);
   pdl_wait();
@@ -1167,13 +1421,18 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   // flag and rho are read alongside (a finished solve only wastes the copies)
   if (tid == 0) {
     sdone = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
-    srho = scal[S_SHIFT];
+    if (!COARSE) srho = scal[S_SHIFT];
+    if (COARSE) {  // y_Kc for the coarse levels, and gdot
+      const int Kc = lv.Kc;
+      C.sky0 = stage_window(&C.bar, sm + coff + cd.o_y[0], Ygl, 8, lv.off[Kc - 1], lv.off[Kc - 1] + lv.n[Kc - 1]);
+      if (mode != M_APPLY) sgd = scal[S_GD];
+    }
   }
   const bool gemv = td.gemv_n > 0;
   if (g == 3 * m1 + 1) {
     const int64_t base = FIRST ? 0 : lv.off[k0 - 1];
     sky0 = stage_window(&bar, sm + td.o_y[0], y0src, 8, base + sa[0], base + sa[0] + sn[0]);
-  } else if (!gemv && (g == 3 * m1 + 2 || g == 3 * m1 + 3)) {
+  } else if (!COARSE && !gemv && (g == 3 * m1 + 2 || g == 3 * m1 + 3)) {
     const bool isz = (g == 3 * m1 + 2);
     const int64_t base = lv.off[k0 + nl - 2] + sa[nl - 1];
     const int v = stage_window(&bar, sm + (isz ? td.o_z[nl - 1] : td.o_w[nl - 1]), isz ? Zg : Wg, 8, base,
@@ -1187,13 +1446,13 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     double* v = reinterpret_cast<double*>(sm + td.o_v);
     const int64_t okc = lv.off[k0 + nl - 2];
     double ys = 0.0, gd = 0.0;
-    for (int j = tid; j < nk; j += TT) {
+    for (int j = tid; j < nk; j += NT) {
       const double yv = __ldcg(Ygl + okc + j);
       v[j] = yv;
       ys += yv;
     }
-    for (int j = tid; j < npart_gd; j += TT) gd += __ldcg(part_gd + j);
-    const double2 sums = block_sum2<TT>(make_double2(ys, gd));
+    for (int j = tid; j < npart_gd; j += NT) gd += __ldcg(part_gd + j);
+    const double2 sums = block_sum2<NT>(make_double2(ys, gd));
     if (tid == 0) {
       v[nk] = sums.y;
       srho_g = lv.c_sum * sums.x / lv.n_tilde;
@@ -1205,7 +1464,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     const int a = sa[nl - 1], cnt = sn[nl - 1], lane = tid & 31, warp = tid >> 5;
     double* zt = reinterpret_cast<double*>(sm + td.o_z[nl - 1]);
     double* wt = reinterpret_cast<double*>(sm + td.o_w[nl - 1]);
-    for (int rr = warp; rr < 2 * cnt; rr += TT / 32) {
+    for (int rr = warp; rr < 2 * cnt; rr += NT / 32) {
       const int row = (rr < cnt) ? a + rr : nk + a + (rr - cnt);
       const double* Mr = Mco + (int64_t)row * (nk + 1);
       double acc = 0.0;
@@ -1221,10 +1480,30 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   __syncthreads();
   const int done = sdone;
   if (gemv && tid == 0) srho = srho_g;
-  if (tid == 0) mbar_arrive(&bar);
+  if (tid == 0) {  // every expect_tx of both barriers precedes (the barrier above)
+    mbar_arrive(&bar);
+    if (COARSE) mbar_arrive(&C.bar);
+  }
   mbar_wait(&bar, 0);
   TRACE(3);
   PHASE(2);
+  if (COARSE) {
+    mbar_wait(&C.bar, 0);
+    if (done) return;
+    double gd = 0.0;
+    if (mode != M_APPLY) gd = (tid == 0) ? sgd : 0.0;
+    else if (tid < 32) {  // apply_R: the partials are summed here
+      const double t = warp_sum_partials(part_gd, npart_gd);
+      gd = (tid == 0) ? t : 0.0;
+    }
+    coarse_table(C, lv, cd, coff);
+    const double* pinv =
+        cd.stage_pinv ? reinterpret_cast<const double*>(sm + coff + cd.o_pinv) + C.skp : pinv_g;
+    coarse_levels(lv, C.tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, coff + cd.o_tt, true);
+    __syncthreads();
+    if (tid == 0) srho = scal[S_SHIFT];  // written by warp 0 above
+    __syncthreads();
+  }
   if (done) return;
 
   // per-level pointer table (one thread per level), so every phase starts
@@ -1237,8 +1516,8 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     e.lo = (t + 1 < nl) ? td.o_lo[t] + 8 * skl[t] : -1;
     e.y = (t == 0) ? td.o_y[0] + 8 * sky0 : (t + 1 < nl ? td.o_y[t] : -1);
     e.nn = (t == 0) ? (FIRST ? -1 : td.o_n[0] + 8 * skn0) : (t + 1 < nl ? td.o_n[t] : -1);
-    e.z = (t == nl - 1) ? td.o_z[t] + 8 * skz : (t >= 1 ? td.o_z[t] : -1);
-    e.w = (t == nl - 1) ? td.o_w[t] + 8 * skw : (t >= 1 ? td.o_w[t] : -1);
+    e.z = (t == nl - 1) ? (COARSE ? coff + cd.o_z[0] + 8 * sa[t] : td.o_z[t] + 8 * skz) : (t >= 1 ? td.o_z[t] : -1);
+    e.w = (t == nl - 1) ? (COARSE ? coff + cd.o_w[0] + 8 * sa[t] : td.o_w[t] + 8 * skw) : (t >= 1 ? td.o_w[t] : -1);
     e.a = sa[t];
     e.cnt = sn[t];
     e.ck = lv.ck[k0 + t];
@@ -1255,7 +1534,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     const int ac = tb[t - 1].a, npar = tb[t].cnt;
     if (nc) {
       #pragma unroll 1
-      for (int i = tid; i < npar; i += TT) {
+      for (int i = tid; i < npar; i += NT) {
         const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
         double y = 0.0, N = 1.0;
         #pragma unroll 1
@@ -1268,7 +1547,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
       }
     } else {  // level-1 children: N = 1 each
       #pragma unroll 1
-      for (int i = tid; i < npar; i += TT) {
+      for (int i = tid; i < npar; i += NT) {
         const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
         double y = yc[c0] + yc[c0 + 1];  // every aggregate has its matched pair
         #pragma unroll 1
@@ -1299,7 +1578,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     const int ac = tb[t].a, npar = tb[t + 1].cnt;
     const double ckk = tb[t].ck;
     #pragma unroll 1
-    for (int i = tid; i < npar; i += TT) {
+    for (int i = tid; i < npar; i += NT) {
       const int lb = -3 * (2 * i + 2);
       block_solve(
           cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
@@ -1324,7 +1603,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
     double* zg = FIRST ? zout + zs * ac : Zg + lv.off[k0 - 1] + ac;
     double* wg = Wg + lv.off[k0 - 1] + ac;
     #pragma unroll 1
-    for (int i = tid; i < npar; i += TT) {
+    for (int i = tid; i < npar; i += NT) {
       const int lb = -3 * (2 * i + 2);
       if (FIRST)
         block_solve(
@@ -1344,7 +1623,7 @@ __global__ void __launch_bounds__(TT) k_tile_down(const __grid_constant__ Lv lv,
   PHASE(5);
   pdl_trigger();
   if (FIRST) {
-    rz = block_sum<TT>(rz);
+    rz = block_sum<NT>(rz);
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) part[tile] = rz;
       if (mode != M_APPLY && warp_last_block(&cnt[C_DOWN])) {
@@ -1470,180 +1749,6 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
   }
 }
 
-// --------------------------------------------------------- coarse kernel
-// Levels Kc..L of the coarse kernel when the top has <= 32 nodes.  Level t
-// (n_{Kc+t} nodes, one per thread) runs on its first W(t) = ceil(n/32) warps
-// only; the barrier before a level spans exactly the warps of the larger of
-// the two levels it separates (a named barrier, __syncwarp for one warp), so
-// the small upper levels cost a warp-level sync instead of a 32-warp one.  The
-// top solve runs on warp 0.  Level Kc goes straight to global memory.
-// Barrier ids: 1 for the up sweep (its warp sets only shrink, so every warp
-// of an instance has left the previous one); one id per down level (2 + t),
-// because a warp that joins the down sweep late arrives at its first barrier
-// while the others are still levels above.
-__device__ __forceinline__ void named_sync(int id, int nw) {
-  if (nw == 1) __syncwarp();
-  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nw * 32) : "memory");
-}
-
-#undef TRACE_KID
-#define TRACE_KID 1
-__device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, char* sm, const double* __restrict__ pinv,
-                                           double* __restrict__ Zg, double* __restrict__ Wg,
-                                           double* __restrict__ zout, double* __restrict__ scal, double gd,
-                                           int mode_in, int o_tt) {
-  constexpr int NW = CT / 32;
-  const int mode = mode_in & 15;
-  const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ double srho;
-  auto W = [&](int t) {  // tb[t].cnt = n_{Kc+t} (shared memory)
-    const int c = (tb[t].cnt + 31) >> 5;
-    return c < 1 ? 1 : (c > NW ? NW : c);
-  };
-  __syncthreads();  // pointer table and staged segments
-  // ---- up: level t on warps [0, W(t))
-  for (int t = 1; t < nl; ++t) {
-    if (t >= 2) {
-      const int wp = W(t - 1);
-      if (warp >= wp) break;
-      named_sync(1, wp);
-    }
-    if (t <= 7) TRACE(6 + t);
-    const int wt = W(t);
-    if (warp < wt) {
-      const int* cp = SMP(const int, tb[t].cp);
-      const double* yc = SMP(const double, tb[t - 1].y);
-      double* yp = SMP(double, tb[t].y);
-      const int np = tb[t].cnt;
-      #pragma unroll 1
-      for (int i = tid; i < np; i += 32 * wt) {
-        double y = 0.0;
-        const int c1 = cp[i + 1];
-        #pragma unroll 1
-        for (int c = cp[i]; c < c1; ++c) y += yc[c];
-        yp[i] = y;
-      }
-    }
-  }
-  // ---- top solve (warp 0)
-  double rz = 0.0;
-  const int ntop = tb[nl - 1].cnt;
-  if (warp == 0) {
-    __syncwarp();
-    const double* yt = SMP(const double, tb[nl - 1].y);
-    const double* Nt = SMP(const double, tb[nl - 1].nn);
-    double ysum = 0.0;
-    #pragma unroll 1
-    for (int i = lane; i < ntop; i += 32) ysum += yt[i];
-    ysum = warp_sum(ysum);
-    gd = warp_sum(gd);
-    const double rho = lv.c_sum * ysum / lv.n_tilde;
-    double* tt = reinterpret_cast<double*>(sm + o_tt);
-    #pragma unroll 1
-    for (int i = lane; i < ntop; i += 32) tt[i] = lv.ck[L] * yt[i] - rho * Nt[i];
-    __syncwarp();
-    double* zt = SMP(double, tb[nl - 1].z);
-    double* wt = SMP(double, tb[nl - 1].w);
-    double nz = 0.0;
-    #pragma unroll 1
-    for (int i = lane; i < ntop; i += 32) {
-      double zi = 0.0;
-      #pragma unroll 1
-      for (int j = 0; j < ntop; ++j) zi += pinv[i * ntop + j] * tt[j];
-      zt[i] = zi;
-      nz += Nt[i] * zi;
-    }
-    nz = warp_sum(nz);
-    const double m = (nz + gd - rho * lv.GN) / lv.n_tilde;
-    #pragma unroll 1
-    for (int i = lane; i < ntop; i += 32) {
-      const double z = zt[i] - m;
-      zt[i] = z;
-      wt[i] = z;
-      if (L == 1) {
-        rz += yt[i] * z;
-        zout[((mode_in & M_ZS2) ? 2 : 1) * i] = z;
-      } else if (nl == 1) {  // the top is level Kc: to global
-        if (mode == M_COLUMN) {
-          Zg[(int64_t)blockIdx.x * 2 * ntop + i] = z;
-          Zg[(int64_t)blockIdx.x * 2 * ntop + ntop + i] = z;
-        } else {
-          Zg[lv.off[Kc - 1] + i] = z;
-          Wg[lv.off[Kc - 1] + i] = z;
-        }
-      }
-    }
-    if (lane == 0) {
-      srho = rho;
-      if (mode != M_COLUMN) scal[S_SHIFT] = rho;
-    }
-    __syncwarp();
-  }
-  TRACE(5);
-  // ---- down: level t on warps [0, W(t)) (W grows as t falls)
-  const double negmu = lv.negmu;
-  for (int t = nl - 2; t >= 0; --t) {
-    const int wt = W(t);
-    if (warp >= wt) continue;
-    named_sync(2 + t, wt);
-    const double rho = srho;
-    const int* cp = SMP(const int, tb[t + 1].cp);
-    const double* ki = SMP(const double, tb[t + 1].ki);
-    const double* zp = SMP(const double, tb[t + 1].z);
-    const double* wp = SMP(const double, tb[t + 1].w);
-    const double* lo = SMP(const double, tb[t].lo);
-    const double* yc = SMP(const double, tb[t].y);
-    const double* nc = SMP(const double, tb[t].nn);
-    double* zc = SMP(double, tb[t].z);
-    double* wc = SMP(double, tb[t].w);
-    const double ckk = tb[t].ck;
-    const int np = tb[t + 1].cnt;
-    const int nk = tb[t].cnt;
-    if (t > 0) {
-      #pragma unroll 1
-      for (int i = tid; i < np; i += 32 * wt) {
-        const int lb = -3 * (2 * i + 2);
-        block_solve(
-            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
-            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
-            [&](int p, double z, double w) { zc[p] = z; wc[p] = w; });
-      }
-    } else if (Kc == 1) {  // level-1 output and (r, R r)
-      const int zs = (mode_in & M_ZS2) ? 2 : 1;
-      #pragma unroll 1
-      for (int i = tid; i < np; i += 32 * wt) {
-        const int lb = -3 * (2 * i + 2);
-        block_solve(
-            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
-            zp[i], negmu * wp[i], [&](int p) { return yc[p] - rho; },
-            [&](int p, double z, double w) { rz += yc[p] * w; zout[zs * p] = w; });
-      }
-    } else {  // level Kc to global: Z, W (or column blockIdx.x of the GEMV map)
-      double* zg = (mode == M_COLUMN) ? Zg + (int64_t)blockIdx.x * 2 * nk : Zg + lv.off[Kc - 1];
-      double* wg = (mode == M_COLUMN) ? zg + nk : Wg + lv.off[Kc - 1];
-      #pragma unroll 1
-      for (int i = tid; i < np; i += 32 * wt) {
-        const int lb = -3 * (2 * i + 2);
-        block_solve(
-            cp[i], cp[i + 1], [&](int j) { return ki[3 * i + j]; }, [&](int p, int j) { return lo[lb + 3 * p + j]; },
-            zp[i], negmu * wp[i], [&](int p) { return ckk * yc[p] - rho * nc[p]; },
-            [&](int p, double z, double w) { zg[p] = z; wg[p] = w; });
-      }
-    }
-  }
-  TRACE(6);
-  pdl_trigger();
-  if (Kc == 1) {
-    rz = block_sum<CT>(rz);
-    if (tid == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
-  }
-}
-
-// Single CTA: levels Kc..L up-sweep, the top solve, levels L..Kc down-sweep,
-// everything staged in / computed into shared memory (layout: CoarseDesc).
-// When Kc == 1 it also produces the level-1 output and (r, R r).
-#undef TRACE_KID
-#define TRACE_KID 1
 __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, const __grid_constant__ CoarseDesc cd,
                                                const int32_t* __restrict__ cptr, const double* __restrict__ kinv,
                                                const double* __restrict__ lof, const double* __restrict__ Nsub,
@@ -1655,10 +1760,8 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
-  __shared__ int sky0, skp, sdone;
-  __shared__ LvlPtr tb[MAXT + 8];
+  __shared__ CoarseState C;
+  __shared__ int sdone;
   // the level table is read level by level; a single CTA would take a cold
   // constant-cache miss at nearly every level, so it is copied to shared
   // memory once, all words in parallel
@@ -1669,50 +1772,24 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
   const Lv& lv = slv;
   const int tid = threadIdx.x;
   TRACE(0);
-  if (tid == 0) mbar_init(&bar, 1);
+  if (tid == 0) mbar_init(&C.bar, 1);
   __syncthreads();
   const int L = lv.L, Kc = lv.Kc, nl = cd.nl;
-  const int64_t n1 = lv.n[0];
-  // segments, one per warp (g = lane * 32 + warp): [0, nl-1) child pointers,
-  // [nl-1, 2nl-2) factors, [2nl-2, 3nl-3) leftover coefficients,
-  // [3nl-3, 4nl-3) subtree sizes, 4nl-3 the top pseudo-inverse; after the
-  // grid dependency 4nl-2: y_Kc
-  const int g = (tid & 31) * (CT / 32) + (tid >> 5);
-  const int m1 = nl - 1;
-  if (g < m1) {
-    const int t = g + 1;
-    const int64_t base = lv.cpo[Kc + t - 2];
-    skc[t] = stage_window<true>(&bar, sm + cd.o_cp[t], cptr, 4, base, base + lv.n[Kc + t - 1] + 1);
-  } else if (g < 2 * m1) {
-    const int t = g - m1 + 1;
-    const int64_t base = 3 * (lv.off[Kc + t - 1] - n1);
-    skk[t] = stage_window<true>(&bar, sm + cd.o_ki[t], kinv, 8, base, base + 3 * lv.n[Kc + t - 1]);
-  } else if (g < 3 * m1) {
-    const int t = g - 2 * m1;
-    const int64_t base = 3 * lv.lo[Kc + t - 1];
-    skl[t] = stage_window<true>(&bar, sm + cd.o_lo[t], lof, 8, base, base + 3 * (lv.n[Kc + t - 1] - 2 * lv.n[Kc + t]));
-  } else if (g < 3 * m1 + nl) {
-    const int t = g - 3 * m1;
-    const int64_t base = lv.off[Kc + t - 1];
-    skn[t] = stage_window<true>(&bar, sm + cd.o_n[t], Nsub, 8, base, base + lv.n[Kc + t - 1]);
-  } else if (g == 3 * m1 + nl && cd.stage_pinv) {
-    const int64_t nt = lv.n[L - 1];
-    skp = stage_window<true>(&bar, sm + cd.o_pinv, pinv_g, 8, 0, nt * nt);
-  }
+  coarse_stage_static<CT>(C, sm, lv, cd, cptr, kinv, lof, Nsub, pinv_g);
   TRACE(1);
   pdl_wait();
   TRACE(2);
   if (tid == 0) sdone = (mode == M_INIT || mode == M_ITER) ? (int)cnt[C_DONE] : 0;
   __syncthreads();
   const int done = sdone;
-  if (g == 3 * m1 + nl + 1 && !done) {
+  if (tid == 0 && !done) {
     // M_COLUMN (setup of the coarse GEMV matrix): CTA j solves for the j-th
     // unit input, whose y_Kc is row j of y0src (n_Kc x n_Kc identity, then 0)
     const int64_t base = (mode == M_COLUMN) ? (int64_t)blockIdx.x * lv.n[Kc - 1] : ((Kc == 1) ? 0 : lv.off[Kc - 1]);
-    sky0 = stage_window(&bar, sm + cd.o_y[0], y0src, 8, base, base + lv.n[Kc - 1]);
+    C.sky0 = stage_window(&C.bar, sm + cd.o_y[0], y0src, 8, base, base + lv.n[Kc - 1]);
   }
   __syncthreads();
-  if (tid == 0) mbar_arrive(&bar);
+  if (tid == 0) mbar_arrive(&C.bar);
   // small top (<= 32 nodes): the levels run on as many warps as they have
   // nodes for, the top solve on warp 0 (so gdot is summed there)
 #ifndef MSP_NO_SMALLTOP
@@ -1734,25 +1811,12 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
   } else {
     for (int i = tid; i < npart; i += CT) gd += __ldcg(part_gd + i);
   }
-  mbar_wait(&bar, 0);
+  mbar_wait(&C.bar, 0);
   TRACE(3);
   if (done) return;
-
-  if (tid < nl) {  // per-level pointer table
-    const int t = tid;
-    LvlPtr e;
-    e.cp = (t >= 1) ? cd.o_cp[t] + 4 * skc[t] : -1;
-    e.ki = (t >= 1) ? cd.o_ki[t] + 8 * skk[t] : -1;
-    e.lo = (t + 1 < nl) ? cd.o_lo[t] + 8 * skl[t] : -1;
-    e.y = cd.o_y[t] + (t == 0 ? 8 * sky0 : 0);
-    e.nn = cd.o_n[t] + 8 * skn[t];
-    e.z = cd.o_z[t];
-    e.w = cd.o_w[t];
-    e.a = 0;
-    e.cnt = (int)lv.n[Kc + t - 1];
-    e.ck = lv.ck[Kc + t];
-    tb[t] = e;
-  }
+  coarse_table(C, lv, cd, 0);
+  LvlPtr* tb = C.tb;
+  const int skp = C.skp;
   if (small_top) {
     const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
     coarse_levels(lv, tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, cd.o_tt);
@@ -2134,8 +2198,10 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     ++h.launches;
     if (dc && i == 0 && !dist_after_tier1_up(h, *dc, st, mbase)) return;  // converged
   }
-  // ---- coarse (folded into the top tier's down kernel in GEMV mode)
-  if (!h.gemv) {
+  // ---- coarse (folded into the top tier's down kernel in GEMV mode, and
+  // into the last tier's down kernel when merged)
+  const bool merged = h.merged_coff > 0 && !dc;
+  if (!h.gemv && !merged) {
     P.begin();
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
     launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
@@ -2172,13 +2238,20 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
                cnt, mode | (dc ? M_DIST : 0), (const double*)h.Mco.p, (const double*)part_gd, npart_up,
-               (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p);
+               (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p, h.cdesc, 0,
+               (const double*)nullptr);
+      else if (merged && i == nt - 1)  // the coarse levels run inside this kernel
+        launch(k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, T.desc,
+               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
+               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
+               (const int4*)T.segs.p, h.cdesc, (int)h.merged_coff, (const double*)h.top_pinv.p);
       else
         launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
-               (const int4*)T.segs.p);
+               (const int4*)T.segs.p, h.cdesc, 0, (const double*)nullptr);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
@@ -2368,6 +2441,26 @@ void alloc_solve_workspace(Handle& h) {
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)h.coarse_smem));
+  // merged last-tier down + coarse kernel (tier k1 == Kc, small top)
+  h.merged_coff = 0;
+  h.merged_smem = 0;
+  {
+    const int L = h.levels, nlc = L - h.Kc + 1;
+    const bool small_top = h.lv[L - 1].n <= 32 && nlc <= 14;
+    if (!std::getenv("MSP_NO_MERGE") && !h.gemv && h.tiers.size() >= 2 && small_top && h.Kc > 1) {
+      auto& T = h.tiers.back();
+      if (!T.generic && T.k1 == h.Kc && T.k0 > 1) {
+        const size_t coff = (T.smem_down + 15) & ~(size_t)15;
+        const size_t tot = coff + h.coarse_smem;
+        if (tot <= 220 * 1024) {
+          MSP_CUDA(cudaFuncSetAttribute((const void*)k_tile_down<false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tot));
+          h.merged_coff = std::max<size_t>(coff, 16);
+          h.merged_smem = h.merged_coff + h.coarse_smem;
+        }
+      }
+    }
+  }
   // fused SpMV + first-tier up: persistent grid no larger than the number of
   // co-resident CTAs (its grid barrier spins)
   h.fuse_grid = 0;
