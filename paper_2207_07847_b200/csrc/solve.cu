@@ -273,6 +273,20 @@ __device__ __forceinline__ double warp_sum_partials(const double* part, int64_t 
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
+// the same for two partial arrays at once (loads of both in flight together)
+__device__ __forceinline__ double2 warp_sum_partials2(const double* pa, const double* pb, int64_t n) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  int64_t i = threadIdx.x & 31;
+  for (; i + 32 < n; i += 64) {
+    a0 += __ldcg(pa + i);
+    b0 += __ldcg(pb + i);
+    a1 += __ldcg(pa + i + 32);
+    b1 += __ldcg(pb + i + 32);
+  }
+  for (; i < n; i += 32) { a0 += __ldcg(pa + i); b0 += __ldcg(pb + i); }
+  return make_double2(warp_sum(a0 + a1), warp_sum(b0 + b1));
+}
+
 // Exact solve of one aggregate of T~: children [s0, s1) (matched pair s0,
 // s0+1, leftovers s0+2..), K(j) the packed K'^{-1} (uu, uv, vv), C(p, j) the
 // leftover coefficients (sigma w_xu / d, sigma w_xv / d, 1 / d):
@@ -817,8 +831,8 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     if (tid < 32) {  // only warp 0 waits on the ticket
       if (tid == 0) { part_rr[tile] = v.x; part_gd[tile] = v.y; }
       if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
-        const double tot = warp_sum_partials(part_rr + tile0, gridDim.x);
-        const double tgd = warp_sum_partials(part_gd + tile0, gridDim.x);  // (H, r) for the coarse kernel
+        const double2 t2 = warp_sum_partials2(part_rr + tile0, part_gd + tile0, gridDim.x);
+        const double tot = t2.x, tgd = t2.y;  // (r, r); (H, r) for the coarse levels
         if (dist) {  // local totals; k_dist_finish runs after the all-reduce
           if (tid == 0) { scal[S_RR] = tot; scal[S_GD] = tgd; cnt[C_UPD] = 0; }
         } else if (tid == 0) {
