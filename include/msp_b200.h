@@ -77,6 +77,8 @@ typedef struct msp_info_t {
   int64_t ntiles;       /* tiles (CTAs) of the first tier                       */
   int32_t ntiers;
   int32_t spmv_grid;    /* CTAs of the L_G product                              */
+  int32_t merged_coarse;  /* 1: the coarse levels run inside the last tier's down
+                             kernel (one copy per CTA), 0: their own kernel   */
 } msp_info_t;
 
 typedef struct msp_report {

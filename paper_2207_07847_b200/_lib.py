@@ -39,7 +39,8 @@ class _Info(ctypes.Structure):
                 ("levels", ctypes.c_int32), ("mwm_rounds", ctypes.c_int32), ("mu", ctypes.c_double),
                 ("setup_ms", ctypes.c_double), ("tile_level", ctypes.c_int32),
                 ("coarse_level", ctypes.c_int32), ("ntiles", ctypes.c_int64),
-                ("ntiers", ctypes.c_int32), ("spmv_grid", ctypes.c_int32)]
+                ("ntiers", ctypes.c_int32), ("spmv_grid", ctypes.c_int32),
+                ("merged_coarse", ctypes.c_int32)]
 
 
 class _Report(ctypes.Structure):

@@ -136,6 +136,7 @@ int msp_info(const msp_handle* H, msp_info_t* out) {
     out->ntiles = nt;
     out->ntiers = (int32_t)h.tiers.size();
     out->spmv_grid = (int32_t)h.spmv_grid;
+    out->merged_coarse = h.merged_coff > 0 ? 1 : 0;
   });
 }
 

@@ -277,3 +277,36 @@ def test_full_size_hierarchy_and_sampled_apply_L(idx, scale):
         ws = g.val[g.rowptr[i]:g.rowptr[i + 1]]
         yi = float(np.sum(ws * (x[i] - x[cols])))
         assert abs(y[i] - yi) <= 1e-12 * max(abs(yi), np.abs(ws).sum() * np.abs(x).max())
+
+
+def test_two_tiers_merged_coarse():
+    """A graph with two tiers of tile kernels, whose last tier's down kernel
+    runs the coarse levels itself (`merged_coarse`): apply_R against the
+    oracle (bar of test_apply_R_msp) and against the separate coarse kernel
+    (MSP_NO_MERGE; the same operator -- only FMA contraction may differ, so
+    within 1e-14), and a PCG solve whose true residual meets rtol."""
+    import os
+    g = G.grid2d(320, 320, "loguniform", 4)
+    s = gpu_setup(g, 0.8, 0, 11)
+    info = s.info()
+    assert info["ntiers"] >= 2 and info["merged_coarse"] == 1, info
+    h = A.build_hierarchy(g, 11)
+    sysm = E.expand_msp_only(g, h, 0.8)
+    r = G.rhs(g.n, 5)
+    z = s.apply_R(dt(r)).cpu().numpy()
+    err = relmax(z, PR.msp(sysm)(r))
+    if err > 1e-12:
+        assert err <= max(1e-12, 50 * weight_sensitivity(sysm, r)), err
+    os.environ["MSP_NO_MERGE"] = "1"
+    try:
+        s2 = gpu_setup(g, 0.8, 0, 11)
+    finally:
+        del os.environ["MSP_NO_MERGE"]
+    assert s2.info()["merged_coarse"] == 0
+    assert relmax(z, s2.apply_R(dt(r)).cpu().numpy()) <= 1e-14
+    b = G.rhs(g.n, 6)
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    assert out["converged"] == 1
+    L = GR.laplacian_of_graph(g)
+    x = out["x"].cpu().numpy()
+    assert np.linalg.norm(b - L @ x) <= 2e-8 * np.linalg.norm(b)
