@@ -44,6 +44,9 @@ constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 #ifndef MSP_PF_DIST
 #define MSP_PF_DIST 1
 #endif
+#ifndef MSP_SPMV_LB
+#define MSP_SPMV_LB 4  // min CTAs/SM of the pipelined SpMV (register budget)
+#endif
 #ifndef MSP_FLAT_G
 #define MSP_FLAT_G 4
 #endif
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 #undef TRACE_KID
 #define TRACE_KID 6
 template <int MW, bool UNIF>
-__global__ void __launch_bounds__(TPB, 4) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
+__global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
                                                       const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
                                                       const int32_t* __restrict__ long_rows,
