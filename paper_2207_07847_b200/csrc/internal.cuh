@@ -150,6 +150,7 @@ struct Handle {
   // [z_Kc; w_Kc] = Mco [y_Kc; gdot], row-major (2 n_Kc) x (n_Kc + 1)
   bool gemv = false;
   DBuf<double> Mco;
+  DBuf<double> Mtop;          // top map (CoarseDesc::topmap_t), row-major (2 n_j) x (n_j + 1)
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
   unsigned fuse_grid = 0;
@@ -227,5 +228,7 @@ void nested_to_expanded(Handle& h, const double* src, double* dst, cudaStream_t 
 Lv make_level_table(const Handle& h);              // setup.cu
 void release_graph(Handle& h);
 void build_coarse_matrix(Handle& h, cudaStream_t st);  // solve.cu
+void build_top_map(Handle& h, cudaStream_t st);        // solve.cu
+CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv);  // setup.cu
 
 }  // namespace msp

@@ -63,6 +63,9 @@ struct CoarseDesc {
   int o_cp[MAXT + 8], o_ki[MAXT + 8], o_lo[MAXT + 8], o_n[MAXT + 8];
   int o_y[MAXT + 8], o_z[MAXT + 8], o_w[MAXT + 8];
   int o_pinv, o_tt;
+  // top map: levels j..L replaced by the dense linear map (y_j, gdot) ->
+  // (z_j, w_j), j = Kc + topmap_t (0: off), n_j = mtop_n, staged at o_mtop
+  int topmap_t, mtop_n, o_mtop;
   int smem;
 };
 

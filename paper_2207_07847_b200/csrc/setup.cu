@@ -1128,13 +1128,16 @@ TierDesc tier_layout(int k0, int nl, int64_t ntiles, const std::vector<int64_t>&
   return d;
 }
 
+}  // namespace
+
+static inline int a16c(int64_t b) { return (int)((b + 15) & ~(int64_t)15); }
 CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv) {
   CoarseDesc d{};
   const int L = h.levels, nl = L - Kc + 1;
   d.nl = nl;
   d.stage_pinv = stage_pinv ? 1 : 0;
   int64_t cur = 0;
-  auto take = [&](int64_t bytes) { const int o = a16(cur); cur = o + bytes; return o; };
+  auto take = [&](int64_t bytes) { const int o = a16c(cur); cur = o + bytes; return o; };
   auto nk = [&](int t) { return h.lv[Kc + t - 1].n; };
   for (int t = 1; t < nl; ++t) {
     d.o_cp[t] = take((nk(t) + 1 + 8) * 4);
@@ -1151,10 +1154,10 @@ CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv) {
   const int64_t ntop = h.lv[L - 1].n;
   d.o_pinv = stage_pinv ? take((ntop * ntop + 2) * 8) : 0;
   d.o_tt = take(ntop * 8);
-  d.smem = a16(cur);
+  d.smem = a16c(cur);
   return d;
 }
-}  // namespace
+
 
 // Tiers and tiles of the solve schedule.
 void build_schedule(Handle& h, cudaStream_t st) {

@@ -1137,7 +1137,10 @@ __device__ __forceinline__ void named_sync(int id, int nw) {
 __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, char* sm, const double* __restrict__ pinv,
                                            double* __restrict__ Zg, double* __restrict__ Wg,
                                            double* __restrict__ zout, double* __restrict__ scal, double gd,
-                                           int mode_in, int o_tt, bool kc_to_smem = false) {
+                                           int mode_in, int o_tt, bool kc_to_smem = false,
+                                           const double* __restrict__ mtop = nullptr, int tj = 0, int nj = 0) {
+  // mtop (shared memory): levels Kc+tj .. L by the dense top map instead of
+  // sweeps and the top solve (build_top_map)
   // kc_to_smem: level Kc stays in shared memory (the merged tier-2 down kernel)
   constexpr int NW = CT / 32;
   const int mode = mode_in & 15;
@@ -1148,8 +1151,11 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
     return c < 1 ? 1 : (c > NW ? NW : c);
   };
   __syncthreads();  // pointer table and staged segments
-  // ---- up: level t on warps [0, W(t))
-  for (int t = 1; t < nl; ++t) {
+  // ---- up: level t on warps [0, W(t)) (up to level Kc+tj with the top map)
+  const int tup = mtop ? tj : nl - 1;
+  __shared__ double sgd;
+  if (mtop && tid == 0) sgd = gd;
+  for (int t = 1; t <= tup; ++t) {
     if (t >= 2) {
       const int wp = W(t - 1);
       if (warp >= wp) break;
@@ -1172,10 +1178,41 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
       }
     }
   }
-  // ---- top solve (warp 0)
+  // ---- top solve (warp 0), or the top map (warps [0, W(tj)))
   double rz = 0.0;
   const int ntop = tb[nl - 1].cnt;
-  if (warp == 0) {
+  if (mtop) {
+    const int wj = W(tj);
+    if (warp < wj) {
+      named_sync(1, wj);  // y at level Kc+tj complete, sgd visible
+      const double* yj = SMP(const double, tb[tj].y);
+      double* zj = SMP(double, tb[tj].z);
+      double* wjs = SMP(double, tb[tj].w);
+      const double g0 = sgd;
+      #pragma unroll 1
+      for (int row = tid; row < 2 * nj; row += 32 * wj) {
+        const double* m = mtop + (int64_t)row * (nj + 1);
+        double a0 = 0.0, a1 = 0.0;
+        int c = 0;
+        #pragma unroll 1
+        for (; c + 1 < nj; c += 2) { a0 += m[c] * yj[c]; a1 += m[c + 1] * yj[c + 1]; }
+        if (c < nj) a0 += m[c] * yj[c];
+        const double v = (a0 + a1) + m[nj] * g0;
+        if (row < nj) zj[row] = v;
+        else wjs[row - nj] = v;
+      }
+      if (warp == 0) {  // rho from the same y (sums are preserved up the tree)
+        double ysum = 0.0;
+        #pragma unroll 1
+        for (int i = lane; i < nj; i += 32) ysum += yj[i];
+        ysum = warp_sum(ysum);
+        if (lane == 0) {
+          srho = lv.c_sum * ysum / lv.n_tilde;
+          if (mode != M_COLUMN) scal[S_SHIFT] = srho;
+        }
+      }
+    }
+  } else if (warp == 0) {
     __syncwarp();
     const double* yt = SMP(const double, tb[nl - 1].y);
     const double* Nt = SMP(const double, tb[nl - 1].nn);
@@ -1229,7 +1266,7 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
   TRACE(5);
   // ---- down: level t on warps [0, W(t)) (W grows as t falls)
   const double negmu = lv.negmu;
-  for (int t = nl - 2; t >= 0; --t) {
+  for (int t = mtop ? tj - 1 : nl - 2; t >= 0; --t) {
     const int wt = W(t);
     if (warp >= wt) continue;
     named_sync(2 + t, wt);
@@ -1296,7 +1333,7 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
 struct CoarseState {
   uint64_t bar;
   int skc[MAXT + 8], skk[MAXT + 8], skl[MAXT + 8], skn[MAXT + 8];
-  int sky0, skp;
+  int sky0, skp, skm;
   LvlPtr tb[MAXT + 8];
 };
 
@@ -1310,7 +1347,8 @@ __device__ __forceinline__ void coarse_stage_static(CoarseState& C, char* smc, c
                                                     const double* __restrict__ kinv,
                                                     const double* __restrict__ lof,
                                                     const double* __restrict__ Nsub,
-                                                    const double* __restrict__ pinv_g) {
+                                                    const double* __restrict__ pinv_g,
+                                                    const double* __restrict__ mtop_g) {
   const int tid = threadIdx.x, L = lv.L, Kc = lv.Kc, nl = cd.nl;
   const int64_t n1 = lv.n[0];
   const int g = (tid & 31) * (NT / 32) + (tid >> 5);
@@ -1335,6 +1373,9 @@ __device__ __forceinline__ void coarse_stage_static(CoarseState& C, char* smc, c
   } else if (g == 3 * m1 + nl && cd.stage_pinv) {
     const int64_t nt = lv.n[L - 1];
     C.skp = stage_window<true>(&C.bar, smc + cd.o_pinv, pinv_g, 8, 0, nt * nt);
+  } else if (g == 3 * m1 + nl + 1 && cd.topmap_t > 0 && mtop_g) {
+    const int64_t nj = cd.mtop_n;
+    C.skm = stage_window<true>(&C.bar, smc + cd.o_mtop, mtop_g, 8, 0, 2 * nj * (nj + 1));
   }
 }
 
@@ -1379,7 +1420,8 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
                                                   int npart_gd, const double* __restrict__ Ygl, int tile0,
                                                   const int4* __restrict__ segs,
                                                   const __grid_constant__ CoarseDesc cd, int coff,
-                                                  const double* __restrict__ pinv_g) {
+                                                  const double* __restrict__ pinv_g,
+                                                  const double* __restrict__ mtop_g) {
   constexpr int NT = COARSE ? CT : TT;
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
@@ -1428,7 +1470,7 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   }
   const int g = (tid & 31) * (NT / 32) + (tid >> 5);  // dynamic segments below
   const int m1 = nl - 1;
-  if (COARSE) coarse_stage_static<NT>(C, sm + coff, lv, cd, cptr, kinv, lof, Nsub, pinv_g);
+  if (COARSE) coarse_stage_static<NT>(C, sm + coff, lv, cd, cptr, kinv, lof, Nsub, pinv_g, mtop_g);
   TRACE(1);
   PHASE(0);
   pdl_wait();
@@ -1516,7 +1558,10 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     coarse_table(C, lv, cd, coff);
     const double* pinv =
         cd.stage_pinv ? reinterpret_cast<const double*>(sm + coff + cd.o_pinv) + C.skp : pinv_g;
-    coarse_levels(lv, C.tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, coff + cd.o_tt, true);
+    const double* mtop = (cd.topmap_t > 0 && mtop_g)
+                             ? reinterpret_cast<const double*>(sm + coff + cd.o_mtop) + C.skm : nullptr;
+    coarse_levels(lv, C.tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, coff + cd.o_tt, true, mtop, cd.topmap_t,
+                  cd.mtop_n);
     __syncthreads();
     if (tid == 0) srho = scal[S_SHIFT];  // written by warp 0 above
     __syncthreads();
@@ -1773,7 +1818,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
                                                double* __restrict__ Zg, double* __restrict__ Wg,
                                                double* __restrict__ zout, const double* __restrict__ part_gd,
                                                int npart, double* __restrict__ scal, unsigned int* __restrict__ cnt,
-                                               int mode_in) {
+                                               int mode_in, const double* __restrict__ mtop_g) {
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
   extern __shared__ __align__(16) char sm[];
@@ -1792,7 +1837,7 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
   if (tid == 0) mbar_init(&C.bar, 1);
   __syncthreads();
   const int L = lv.L, Kc = lv.Kc, nl = cd.nl;
-  coarse_stage_static<CT>(C, sm, lv, cd, cptr, kinv, lof, Nsub, pinv_g);
+  coarse_stage_static<CT>(C, sm, lv, cd, cptr, kinv, lof, Nsub, pinv_g, mode == M_COLUMN ? nullptr : mtop_g);
   TRACE(1);
   pdl_wait();
   TRACE(2);
@@ -1836,7 +1881,9 @@ __global__ void __launch_bounds__(CT) k_coarse(const __grid_constant__ Lv lv_p, 
   const int skp = C.skp;
   if (small_top) {
     const double* pinv = cd.stage_pinv ? reinterpret_cast<const double*>(sm + cd.o_pinv) + skp : pinv_g;
-    coarse_levels(lv, tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, cd.o_tt);
+    const bool map = cd.topmap_t > 0 && mode != M_COLUMN && mtop_g;
+    const double* mtop = map ? reinterpret_cast<const double*>(sm + cd.o_mtop) + C.skm : nullptr;
+    coarse_levels(lv, tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, cd.o_tt, false, mtop, cd.topmap_t, cd.mtop_n);
     return;
   }
   // ---- up
@@ -2223,7 +2270,8 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
     const double* y0 = (h.Kc == 1) ? r : h.Y.p;
     launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
            (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
-           y0, h.Z.p, h.W.p, z, (const double*)part_gd, npart_up, scal, cnt, mode | (dc ? M_DIST : 0));
+           y0, h.Z.p, h.W.p, z, (const double*)part_gd, npart_up, scal, cnt, mode | (dc ? M_DIST : 0),
+           (const double*)h.Mtop.p);
     P.end(PC_COARSE);
     ++h.launches;
   }
@@ -2256,19 +2304,20 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
                cnt, mode | (dc ? M_DIST : 0), (const double*)h.Mco.p, (const double*)part_gd, npart_up,
                (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p, h.cdesc, 0,
-               (const double*)nullptr);
+               (const double*)nullptr, (const double*)nullptr);
       else if (merged && i == nt - 1)  // the coarse levels run inside this kernel
         launch(k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
-               (const int4*)T.segs.p, h.cdesc, (int)h.merged_coff, (const double*)h.top_pinv.p);
+               (const int4*)T.segs.p, h.cdesc, (int)h.merged_coff, (const double*)h.top_pinv.p,
+               (const double*)h.Mtop.p);
       else
         launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
-               (const int4*)T.segs.p, h.cdesc, 0, (const double*)nullptr);
+               (const int4*)T.segs.p, h.cdesc, 0, (const double*)nullptr, (const double*)nullptr);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
@@ -2402,10 +2451,51 @@ void build_coarse_matrix(Handle& h, cudaStream_t st) {
   launch(k_coarse, (unsigned)(nk + 1), CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
          (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
          (const double*)E.p, C.p, C.p, (double*)nullptr, (const double*)nullptr, 0, h.scal.p, h.counters.p,
-         (int)M_COLUMN);
+         (int)M_COLUMN, (const double*)nullptr);
   k_transpose<<<grid_for(2 * nk * (nk + 1)), TPB, 0, st>>>(2 * nk, nk + 1, C.p, h.Mco.p);
   MSP_LAUNCH_CHECK();
   MSP_CUDA(cudaStreamSynchronize(st));
+}
+
+// Top map: when a coarse level j (Kc < j <= L-2) has at most 48 nodes, the
+// levels j..L -- up-sweep, top solve, down-sweep -- are one linear map
+// (y_j, gdot) -> (z_j, w_j) (the coarse GEMV idea of DESIGN.md, restricted to
+// the few top levels, where each output is a sum of at most 49 products, not
+// ~300): built here column by column by the coarse kernel itself (one CTA per
+// unit input) and applied in coarse_levels by a small GEMV from shared memory.
+void build_top_map(Handle& h, cudaStream_t st) {
+  h.cdesc.topmap_t = 0;
+  if (std::getenv("MSP_NO_TOPMAP") || h.gemv) return;
+  const int L = h.levels, Kc = h.Kc, nl = L - Kc + 1;
+  if (!(h.lv[L - 1].n <= 32 && nl <= 14)) return;  // the small-top coarse path only
+  int j = 0;
+  for (int k = Kc + 1; k <= L - 2; ++k)
+    if (h.lv[k - 1].n <= 48) { j = k; break; }
+  if (j == 0) return;
+  const int64_t nj = h.lv[j - 1].n;
+  const bool stage_pinv = h.lv[L - 1].n <= 32;
+  const CoarseDesc cdj = coarse_desc(h, j, stage_pinv);
+  Lv lvj = make_level_table(h);
+  lvj.Kc = j;
+  DBuf<double> E, C;
+  E.alloc((nj + 1) * nj + 8);
+  C.alloc(2 * nj * (nj + 1) + 8);
+  h.Mtop.alloc(2 * nj * (nj + 1) + 8);
+  k_unit_rows<<<grid_for((nj + 1) * nj), TPB, 0, st>>>(nj, E.p);
+  MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max<size_t>(h.coarse_smem, cdj.smem)));
+  launch(k_coarse, (unsigned)(nj + 1), CT, (size_t)cdj.smem, st, lvj, cdj, (const int32_t*)h.cptr.p,
+         (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
+         (const double*)E.p, C.p, C.p, (double*)nullptr, (const double*)nullptr, 0, h.scal.p, h.counters.p,
+         (int)M_COLUMN, (const double*)nullptr);
+  k_transpose<<<grid_for(2 * nj * (nj + 1)), TPB, 0, st>>>(2 * nj, nj + 1, C.p, h.Mtop.p);
+  MSP_LAUNCH_CHECK();
+  MSP_CUDA(cudaStreamSynchronize(st));
+  h.cdesc.topmap_t = j - Kc;
+  h.cdesc.mtop_n = (int)nj;
+  h.cdesc.o_mtop = (int)((h.cdesc.smem + 15) & ~15);
+  h.cdesc.smem = (int)((h.cdesc.o_mtop + (2 * nj * (nj + 1) + 2) * 8 + 15) & ~(int64_t)15);
+  h.coarse_smem = h.cdesc.smem;
 }
 
 void release_graph(Handle& h) {
@@ -2447,6 +2537,7 @@ void alloc_solve_workspace(Handle& h) {
   h.scal.alloc(S_NSCAL);
   MSP_CUDA(cudaMemset(h.counters.p, 0, C_NCNT * sizeof(unsigned)));
   MSP_CUDA(cudaMemset(h.scal.p, 0, S_NSCAL * sizeof(double)));
+  build_top_map(h, 0);  // may extend the coarse layout: before the attributes below
   size_t up = 0, down = 0;
   for (auto& T : h.tiers) { up = std::max(up, T.smem_up); down = std::max(down, T.smem_down); }
   for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>})
