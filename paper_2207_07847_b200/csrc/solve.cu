@@ -47,6 +47,9 @@ constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 #ifndef MSP_SPMV_LB
 #define MSP_SPMV_LB 4  // min CTAs/SM of the pipelined SpMV (register budget)
 #endif
+#ifndef MSP_EARLY
+#define MSP_EARLY 1  // measured: 1 (tier-2 up triggers at its start) -1.6 us; other bits neutral or worse
+#endif
 #ifndef MSP_FLAT_G
 #define MSP_FLAT_G 4
 #endif
@@ -498,6 +501,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
                                                       double* __restrict__ part, double* __restrict__ scal,
                                                       unsigned int* __restrict__ cnt) {
   // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
+  if ((MSP_EARLY & 16) != 0) pdl_trigger();
   TRACE(0);
 #ifndef MSP_NO_PF_PRE
   if (UNIF && (threadIdx.x & 31) == 0) {  // constant streams of the first slices, before the dependency
@@ -734,6 +738,10 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   const int tile = (mode_in & M_DIST) ? tA : blockIdx.x;  // partial-sum slot
   const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // early trigger (MSP_EARLY bit 1: tier >= 2 up, bit 2: first-tier up): the
+  // next kernel's CTAs may launch and stage their constants now; its
+  // griddepcontrol.wait still waits for this whole grid
+  if ((FIRST ? (MSP_EARLY & 2) : (MSP_EARLY & 1)) != 0) pdl_trigger();
   TRACE(0);
   PHASE_START();
   if (tid == 0) {
@@ -1316,7 +1324,7 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
     }
   }
   TRACE(6);
-  pdl_trigger();
+  if (!kc_to_smem || (MSP_EARLY & 32) == 0) pdl_trigger();
   if (Kc == 1) {
     rz = block_sum<CT>(rz);
     if (tid == 0 && mode != M_APPLY) finish_rz(rz, scal, mode);
@@ -1436,6 +1444,7 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
+  if ((COARSE ? (MSP_EARLY & 4) : FIRST ? (MSP_EARLY & 8) : (MSP_EARLY & 4)) != 0) pdl_trigger();
   TRACE(0);
   PHASE_START();
   if (tid == 0) {
