@@ -66,6 +66,7 @@ struct CoarseDesc {
   // top map: levels j..L replaced by the dense linear map (y_j, gdot) ->
   // (z_j, w_j), j = Kc + topmap_t (0: off), n_j = mtop_n, staged at o_mtop
   int topmap_t, mtop_n, o_mtop;
+  int overlap;  // merged kernel: coarse levels on warps 0..15 while warps 16..31 recompute the tile
   int smem;
 };
 

@@ -1146,11 +1146,13 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
                                            double* __restrict__ Zg, double* __restrict__ Wg,
                                            double* __restrict__ zout, double* __restrict__ scal, double gd,
                                            int mode_in, int o_tt, bool kc_to_smem = false,
-                                           const double* __restrict__ mtop = nullptr, int tj = 0, int nj = 0) {
+                                           const double* __restrict__ mtop = nullptr, int tj = 0, int nj = 0,
+                                           int nwl = CT / 32) {
+  // nwl: the warps [0, nwl) that run the coarse levels (the others are busy)
   // mtop (shared memory): levels Kc+tj .. L by the dense top map instead of
   // sweeps and the top solve (build_top_map)
   // kc_to_smem: level Kc stays in shared memory (the merged tier-2 down kernel)
-  constexpr int NW = CT / 32;
+  const int NW = nwl;
   const int mode = mode_in & 15;
   const int L = lv.L, Kc = lv.Kc, nl = L - Kc + 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ double srho;
@@ -1158,7 +1160,8 @@ __device__ __forceinline__ void coarse_levels(const Lv& lv, const LvlPtr* tb, ch
     const int c = (tb[t].cnt + 31) >> 5;
     return c < 1 ? 1 : (c > NW ? NW : c);
   };
-  __syncthreads();  // pointer table and staged segments
+  if (NW == CT / 32) __syncthreads();  // pointer table and staged segments
+  else named_sync(1, NW);
   // ---- up: level t on warps [0, W(t)) (up to level Kc+tj with the top map)
   const int tup = mtop ? tj : nl - 1;
   __shared__ double sgd;
@@ -1555,32 +1558,9 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   mbar_wait(&bar, 0);
   TRACE(3);
   PHASE(2);
-  if (COARSE) {
-    mbar_wait(&C.bar, 0);
-    if (done) return;
-    double gd = 0.0;
-    if (mode != M_APPLY) gd = (tid == 0) ? sgd : 0.0;
-    else if (tid < 32) {  // apply_R: the partials are summed here
-      const double t = warp_sum_partials(part_gd, npart_gd);
-      gd = (tid == 0) ? t : 0.0;
-    }
-    coarse_table(C, lv, cd, coff);
-    const double* pinv =
-        cd.stage_pinv ? reinterpret_cast<const double*>(sm + coff + cd.o_pinv) + C.skp : pinv_g;
-    const double* mtop = (cd.topmap_t > 0 && mtop_g)
-                             ? reinterpret_cast<const double*>(sm + coff + cd.o_mtop) + C.skm : nullptr;
-    coarse_levels(lv, C.tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, coff + cd.o_tt, true, mtop, cd.topmap_t,
-                  cd.mtop_n);
-    __syncthreads();
-    if (tid == 0) srho = scal[S_SHIFT];  // written by warp 0 above
-    __syncthreads();
-  }
-  if (done) return;
-
   // per-level pointer table (one thread per level), so every phase starts
   // with a handful of independent shared-memory loads
-  if (tid < nl) {
-    const int t = tid;
+  auto build_table = [&](int t) {
     LvlPtr e;
     e.cp = (t >= 1) ? td.o_cp[t] + 4 * skc[t] : -1;
     e.ki = (t >= 1) ? td.o_ki[t] + 8 * skk[t] : -1;
@@ -1593,40 +1573,80 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     e.cnt = sn[t];
     e.ck = lv.ck[k0 + t];
     tb[t] = e;
-  }
-  // ---- recompute y and N of levels k0+1 .. k1-1
-  for (int t = 1; t + 1 < nl; ++t) {
-    __syncthreads();
-    const int* cp = SMP(const int, tb[t].cp);
-    const double* yc = SMP(const double, tb[t - 1].y);
-    const double* nc = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
-    double* yp = SMP(double, tb[t].y);
-    double* np = SMP(double, tb[t].nn);
-    const int ac = tb[t - 1].a, npar = tb[t].cnt;
-    if (nc) {
-      #pragma unroll 1
-      for (int i = tid; i < npar; i += NT) {
-        const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
-        double y = 0.0, N = 1.0;
+  };
+  // ---- recompute y and N of levels k0+1 .. k1-1 (threads base, base +
+  // stride, ...; sync() before every level)
+  auto recompute = [&](int base, int stride, auto sync) {
+    for (int t = 1; t + 1 < nl; ++t) {
+      sync();
+      const int* cp = SMP(const int, tb[t].cp);
+      const double* yc = SMP(const double, tb[t - 1].y);
+      const double* nc = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
+      double* yp = SMP(double, tb[t].y);
+      double* np = SMP(double, tb[t].nn);
+      const int ac = tb[t - 1].a, npar = tb[t].cnt;
+      if (nc) {
         #pragma unroll 1
-        for (int c = c0; c < c1; ++c) {
-          y += yc[c];
-          N += nc[c];
+        for (int i = base; i < npar; i += stride) {
+          const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
+          double y = 0.0, N = 1.0;
+          #pragma unroll 1
+          for (int c = c0; c < c1; ++c) {
+            y += yc[c];
+            N += nc[c];
+          }
+          yp[i] = y;
+          np[i] = N;
         }
-        yp[i] = y;
-        np[i] = N;
-      }
-    } else {  // level-1 children: N = 1 each
-      #pragma unroll 1
-      for (int i = tid; i < npar; i += NT) {
-        const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
-        double y = yc[c0] + yc[c0 + 1];  // every aggregate has its matched pair
+      } else {  // level-1 children: N = 1 each
         #pragma unroll 1
-        for (int c = c0 + 2; c < c1; ++c) y += yc[c];
-        yp[i] = y;
-        np[i] = (double)(1 + c1 - c0);
+        for (int i = base; i < npar; i += stride) {
+          const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
+          double y = yc[c0] + yc[c0 + 1];  // every aggregate has its matched pair
+          #pragma unroll 1
+          for (int c = c0 + 2; c < c1; ++c) y += yc[c];
+          yp[i] = y;
+          np[i] = (double)(1 + c1 - c0);
+        }
       }
     }
+  };
+  bool recomputed = false;
+  if (COARSE) {
+    mbar_wait(&C.bar, 0);
+    if (done) return;
+    double gd = 0.0;
+    if (mode != M_APPLY) gd = (tid == 0) ? sgd : 0.0;
+    else if (tid < 32) {  // apply_R: the partials are summed here
+      const double t = warp_sum_partials(part_gd, npart_gd);
+      gd = (tid == 0) ? t : 0.0;
+    }
+    // overlap: warps 16..31 recompute the tile's levels (barrier id 15)
+    // while warps 0..15 run the coarse levels (ids 1 .. nl_c < 15)
+    const bool ovl = cd.overlap != 0;
+    const int warp_ = tid >> 5;
+    if (ovl && warp_ >= 16) {
+      const int u = tid - 512;
+      if (u < nl) build_table(u);
+      recompute(u, NT - 512, [&] { named_sync(15, 16); });
+    } else {
+      coarse_table(C, lv, cd, coff);
+      const double* pinv =
+          cd.stage_pinv ? reinterpret_cast<const double*>(sm + coff + cd.o_pinv) + C.skp : pinv_g;
+      const double* mtop = (cd.topmap_t > 0 && mtop_g)
+                               ? reinterpret_cast<const double*>(sm + coff + cd.o_mtop) + C.skm : nullptr;
+      coarse_levels(lv, C.tb, sm, pinv, Zg, Wg, zout, scal, gd, mode_in, coff + cd.o_tt, true, mtop, cd.topmap_t,
+                    cd.mtop_n, ovl ? 16 : NT / 32);
+    }
+    __syncthreads();
+    if (tid == 0) srho = scal[S_SHIFT];  // written by warp 0 above
+    recomputed = ovl;
+    __syncthreads();
+  }
+  if (done) return;
+  if (!recomputed) {
+    if (tid < nl) build_table(tid);
+    recompute(tid, NT, [] { __syncthreads(); });
   }
   TRACE(4);
   PHASE(3);
@@ -2574,6 +2594,9 @@ void alloc_solve_workspace(Handle& h) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tot));
           h.merged_coff = std::max<size_t>(coff, 16);
           h.merged_smem = h.merged_coff + h.coarse_smem;
+          // coarse levels on 16 warps beside the tile recompute when every
+          // coarse level fits them (n_Kc <= 512)
+          h.cdesc.overlap = (!std::getenv("MSP_NO_OVERLAP") && h.lv[h.Kc - 1].n <= 512) ? 1 : 0;
         }
       }
     }
