@@ -51,7 +51,7 @@ constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 #define MSP_EARLY 1  // measured: 1 (tier-2 up triggers at its start) -1.6 us; other bits neutral or worse
 #endif
 #ifndef MSP_FLAT_G
-#define MSP_FLAT_G 4
+#define MSP_FLAT_G 8  // lanes per level-k1 node in the up kernels (2 / 4 / 8 / 16 / 32 measured; 8 best)
 #endif
 #ifndef MSP_CT
 #define MSP_CT 1024
@@ -788,7 +788,42 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   TRACE(4);
   PHASE(2);
   if (done) return;
-  if (FIRST) {  // level-1 update from shared memory; r_new in place of r (it is y_1)
+  constexpr int FG = MSP_FLAT_G;
+  const int sub = tid & (FG - 1);
+  if (FIRST && nl > 1) {
+    // one pass: FG lanes per level-k1 node update its level-1 descendants
+    // (r -= alpha q), accumulate (r, r), (H, r) and the node's sum y_k1
+    const double alpha = salpha;
+    const int a1 = sa0, np = sn1;
+    double* rs = y0 + skr;
+    const double* qs = reinterpret_cast<const double*>(sm + td.o_uq) + skq;
+    const double* hs = reinterpret_cast<const double*>(sm + td.o_uh) + skh;
+    const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
+    double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
+    #pragma unroll 1
+    for (int base = 0; base < np; base += TT / FG) {  // block-uniform trip count
+      const int i = base + tid / FG;
+      double y = 0.0;
+      if (i < np) {
+        const int c1 = f[i + 1] - a1;
+        #pragma unroll 1
+        for (int c = f[i] - a1 + sub; c < c1; c += FG) {
+          double ri = rs[c];
+          if (mode == M_ITER) {
+            ri -= alpha * qs[c];
+            r[a1 + c] = ri;
+          }
+          rr += ri * ri;
+          gd += hs[c] * ri;
+          y += ri;
+        }
+      }
+#pragma unroll
+      for (int o = FG / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (sub == 0 && i < np) yp[i] = y;
+    }
+    PHASE(3);
+  } else if (FIRST) {  // a level-1-only tier: the update alone
     const double alpha = salpha;
     const int a1 = sa0, n1 = sn0;
     double* rs = y0 + skr;
@@ -798,25 +833,19 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
       double ri = rs[i];
       if (mode == M_ITER) {
         ri -= alpha * qs[i];
-        rs[i] = ri;
         r[a1 + i] = ri;
       }
       rr += ri * ri;
       gd += hs[i] * ri;
     }
-    if (tid == 0) sky0 = skr;
-  }
-  PHASE(3);
-  if (nl > 1) {
-    __syncthreads();
+    PHASE(3);
+  } else if (nl > 1) {
     const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
     const double* yc = y0 + sky0;
     const int a0 = sa0, np = sn1;
     double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
     // FG lanes per level-k1 node, two partial sums per lane, then a
     // butterfly over the group (fixed order)
-    constexpr int FG = MSP_FLAT_G;
-    const int sub = tid & (FG - 1);
     for (int base = 0; base < np; base += TT / FG) {  // block-uniform trip count
       const int i = base + tid / FG;
       double ya = 0.0, yb = 0.0;
