@@ -1606,7 +1606,52 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   // ---- recompute y and N of levels k0+1 .. k1-1 (threads base, base +
   // stride, ...; sync() before every level)
   auto recompute = [&](int base, int stride, auto sync) {
+#ifndef MSP_NO_RECOMP2
+    // two levels per step where both need recomputing: a thread takes a
+    // level-(t+1) parent, forms y, N of each child c (level t) from c's
+    // children and sums them -- the same additions in the same order, one
+    // barrier fewer
+    int t = 1;
+    for (; t + 2 < nl; t += 2) {
+      sync();
+      const int* cp1 = SMP(const int, tb[t].cp);
+      const int* cp2 = SMP(const int, tb[t + 1].cp);
+      const double* yg = SMP(const double, tb[t - 1].y);
+      const double* ng = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
+      double* yc = SMP(double, tb[t].y);
+      double* nc = SMP(double, tb[t].nn);
+      double* yp = SMP(double, tb[t + 1].y);
+      double* np = SMP(double, tb[t + 1].nn);
+      const int ag = tb[t - 1].a, ac = tb[t].a, npar = tb[t + 1].cnt;
+      #pragma unroll 1
+      for (int i = base; i < npar; i += stride) {
+        const int c0 = cp2[i] - ac, c1 = cp2[i + 1] - ac;
+        double y2 = 0.0, N2 = 1.0;
+        #pragma unroll 1
+        for (int c = c0; c < c1; ++c) {
+          const int g0 = cp1[c] - ag, g1 = cp1[c + 1] - ag;
+          double y = 0.0, N = 1.0;
+          if (ng) {
+            #pragma unroll 1
+            for (int gg = g0; gg < g1; ++gg) { y += yg[gg]; N += ng[gg]; }
+          } else {
+            #pragma unroll 1
+            for (int gg = g0; gg < g1; ++gg) y += yg[gg];
+            N = (double)(1 + g1 - g0);
+          }
+          yc[c] = y;
+          nc[c] = N;
+          y2 += y;
+          N2 += N;
+        }
+        yp[i] = y2;
+        np[i] = N2;
+      }
+    }
+    for (; t + 1 < nl; ++t) {
+#else
     for (int t = 1; t + 1 < nl; ++t) {
+#endif
       sync();
       const int* cp = SMP(const int, tb[t].cp);
       const double* yc = SMP(const double, tb[t - 1].y);
