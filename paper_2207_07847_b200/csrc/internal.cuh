@@ -153,8 +153,7 @@ struct Handle {
   DBuf<double> Mtop;          // top map (CoarseDesc::topmap_t), row-major (2 n_j) x (n_j + 1)
   std::vector<double> ck;     // c(k) = sum_{j<k} (-mu)^j, k = 0..L (ck[0] unused)
   unsigned spmv_grid = 1;
-  unsigned fuse_grid = 0;
-  size_t merged_coff = 0, merged_smem = 0;  // merged last-tier down + coarse kernel (0: off)  // grid of the fused SpMV + first-tier up kernel (0: not used)
+  size_t merged_coff = 0, merged_smem = 0;  // merged last-tier down + coarse kernel (0: off)
 
   // ---- PEGP (built lazily on first use, pegp.cu)
   bool pegp_ready = false;

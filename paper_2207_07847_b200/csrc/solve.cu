@@ -61,7 +61,7 @@ constexpr int CT = MSP_CT;    // coarse kernel (single CTA)
 // device scalar slots
 enum { S_RHO = 0, S_PQ, S_ALPHA, S_RR, S_GD, S_BETA, S_TOL2, S_BB, S_SHIFT, S_RTOL2, S_RZ, S_NSCAL };
 // counter slots
-enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_GEN, C_NCNT };
+enum { C_SPMV = 0, C_UPD, C_DOWN, C_DONE, C_IT, C_NCNT };
 // sweep modes
 enum { M_APPLY = 0, M_INIT = 1, M_ITER = 2, M_COLUMN = 3 };
 // multi-GPU: local totals only (the caller all-reduces, k_dist_finish derives)
@@ -888,268 +888,6 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
 #ifdef MSP_TRACE
   if (threadIdx.x == 0) atomicAdd(&g_phase[TRACE_KID][15], 1ull);
 #endif
-  TRACE_END();
-}
-
-// ------------------------------------------- fused SpMV + first-tier up
-// One PCG iteration's q = L p and the first tier's up kernel in one grid,
-// separated by a grid-wide barrier (alpha = rho / (p, q) needs every row):
-//   phase 1: the SpMV of k_spmv_pipe (grid-stride over SELL slices), q to
-//            global (it stays in L2), the (p, q) partials and the ticket;
-//            the last CTA derives alpha and bumps the generation counter;
-//   phase 2: every CTA takes groups of `up_group` first-tier tiles
-//            (persistent loop): r = r - alpha q, (r, r), (H, r) and y_k1,
-//            as k_tile_up<true>.
-// The r and H windows of a CTA's first group are staged by TMA before the
-// grid dependency resolves, so they arrive during phase 1.  The grid never
-// exceeds the co-resident CTA count (checked at setup), so the spin in the
-// barrier cannot starve an unscheduled CTA.
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-#undef TRACE_KID
-#define TRACE_KID 7
-template <int MW, bool UNIF>
-__global__ void __launch_bounds__(TPB, 4) k_spmv_up(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
-                                                    const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                                    const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
-                                                    const int32_t* __restrict__ long_rows,
-                                                    const int32_t* __restrict__ rowptr,
-                                                    const int32_t* __restrict__ col, const double* __restrict__ w,
-                                                    const double2* __restrict__ zp, double* __restrict__ zpout,
-                                                    double* __restrict__ q, double* __restrict__ x,
-                                                    double* __restrict__ part, const __grid_constant__ Lv lv,
-                                                    const __grid_constant__ TierDesc td,
-                                                    const int32_t* __restrict__ tstart,
-                                                    const int32_t* __restrict__ firstk0, double* __restrict__ r,
-                                                    const double* __restrict__ H, double* __restrict__ Yg,
-                                                    double* __restrict__ part_rr, double* __restrict__ part_gd,
-                                                    double* __restrict__ scal, unsigned int* __restrict__ cnt) {
-  extern __shared__ __align__(16) char sm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ int sa0, sn0, sa1, sn1, skf, skr, skq, skh;
-  __shared__ unsigned sgen;
-  __shared__ double salpha;
-  const int tid = threadIdx.x;
-  const int nl = td.nl, nt1 = td.ntiles + 1, G = td.up_group;
-  const int ngroups = (td.ntiles + G - 1) / G;
-  TRACE(0);
-  // stage (thread 0) the windows of group gi: firstk0 and H always, r when
-  // `with_r`, q when `with_q`
-  auto stage = [&](int gi, bool with_r, bool with_q) {
-    const int tA = gi * G, tB = min(tA + G, td.ntiles);
-    sa0 = tstart[tA];
-    sn0 = tstart[tB] - sa0;
-    if (nl > 1) {
-      sa1 = tstart[(nl - 1) * nt1 + tA];
-      sn1 = tstart[(nl - 1) * nt1 + tB] - sa1;
-      skf = stage_window<true>(&bar, sm + td.o_uf, firstk0, 4, sa1, (int64_t)sa1 + sn1 + 1);
-    }
-    if (sn0 > 0) {
-      skh = stage_window<true>(&bar, sm + td.o_uh, H, 8, sa0, (int64_t)sa0 + sn0);
-      if (with_r) skr = stage_window(&bar, sm + td.o_uy0, r, 8, sa0, (int64_t)sa0 + sn0);
-      if (with_q) skq = stage_window(&bar, sm + td.o_uq, q, 8, sa0, (int64_t)sa0 + sn0);
-    }
-  };
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    if ((int)blockIdx.x < ngroups) stage(blockIdx.x, true, false);  // r: written two launches back
-  }
-  pdl_wait();
-  TRACE(1);
-  if (cnt[C_DONE]) {  // uniform: set before this launch
-    if (tid == 0) mbar_arrive(&bar);
-    mbar_wait(&bar, 0);
-    return;
-  }
-  // ---------------- phase 1: q = L p (as k_spmv_pipe)
-  {
-    const double beta = scal[S_BETA];
-    const double alpha_old = scal[S_ALPHA];
-    const int lane = tid & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)TPB + tid) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * TPB) >> 5;
-    double d = 0.0;
-    int64_t s = warp;
-    int64_t b0 = 0, b1 = 0;
-    if (UNIF) { b0 = s * 32 * MW; b1 = b0 + 32 * MW; }
-    else if (s < nslices) { b0 = sptr[s]; b1 = sptr[s + 1]; }
-    int32_t jc[MW];
-    double wc[MW];
-    double po = 0.0, zr = 0.0;
-    uint32_t mk = 0;
-    auto load_B = [&](int64_t ss, int64_t bb0, int64_t bb1) {
-      const int wd = UNIF ? MW : (int)((bb1 - bb0) >> 5);
-      const int64_t rr_ = ss * 32 + lane;
-#pragma unroll
-      for (int k = 0; k < MW; ++k) {
-        if (k < wd) {
-          jc[k] = __ldcs(scol + bb0 + k * 32 + lane);
-          wc[k] = __ldcs(sw + bb0 + k * 32 + lane);
-        }
-      }
-      mk = smask[ss];
-      if (rr_ < n) { const double2 v = zp[rr_]; zr = v.x; po = v.y; }
-    };
-    if (s < nslices) load_B(s, b0, b1);
-    while (s < nslices) {
-      const int64_t s1 = s + nwarps;
-      int64_t n0 = 0, n1 = 0;
-      if (UNIF) { n0 = s1 * 32 * MW; n1 = n0 + 32 * MW; }
-      else if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }
-      const int wd = UNIF ? MW : (int)((b1 - b0) >> 5);
-      const int64_t row = s * 32 + lane;
-      const double pi = zr + beta * po;
-      double g[MW];
-#pragma unroll
-      for (int k = 0; k < MW; ++k)
-        if (k < wd) {
-          const double2 v = zp[jc[k]];
-          g[k] = v.x + beta * v.y;
-        }
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < MW; ++k)
-        if (k < wd) acc += wc[k] * (pi - g[k]);
-      if (row < n && !((mk >> lane) & 1u)) {
-        q[row] = acc;
-        zpout[2 * row + 1] = pi;
-        __stcs(x + row, __ldcs(x + row) + alpha_old * po);
-        d += pi * acc;
-      }
-      s = s1;
-      b0 = n0;
-      b1 = n1;
-      if (s < nslices) load_B(s, b0, b1);
-    }
-    for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
-      const int64_t row = long_rows[i];
-      const double2 vr = zp[row];
-      const double pr = vr.y;
-      const double pi = vr.x + beta * pr;
-      double acc = row_dot<32>(col, w, rowptr[row], rowptr[row + 1], lane, pi, [&](int32_t j) {
-        const double2 v = zp[j];
-        return v.x + beta * v.y;
-      });
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        q[row] = acc;
-        zpout[2 * row + 1] = pi;
-        x[row] += alpha_old * pr;
-        d += pi * acc;
-      }
-    }
-    for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
-      const int64_t row = long_rows[nlong + i];
-      const double2 vr = zp[row];
-      const double pr = vr.y;
-      const double pi = vr.x + beta * pr;
-      double acc = row_dot<TPB>(col, w, rowptr[row], rowptr[row + 1], threadIdx.x, pi, [&](int32_t j) {
-        const double2 v = zp[j];
-        return v.x + beta * v.y;
-      });
-      acc = block_sum<TPB>(acc);
-      if (threadIdx.x == 0) {
-        q[row] = acc;
-        zpout[2 * row + 1] = pi;
-        x[row] += alpha_old * pr;
-        d += pi * acc;
-      }
-    }
-    TRACE(2);
-    // ---------------- grid barrier: the last CTA forms alpha
-    const double bs = block_sum<TPB>(d);  // ends with __syncthreads: q of this CTA stored
-    if (tid < 32) {
-      if (tid == 0) {
-        sgen = ld_acquire(&cnt[C_GEN]);  // before the ticket
-        part[blockIdx.x] = bs;
-      }
-      if (warp_last_block(&cnt[C_SPMV])) {
-        const double pq = warp_sum_partials(part, gridDim.x);
-        if (tid == 0) {
-          const double a = scal[S_RHO] / pq;
-          scal[S_PQ] = pq;
-          scal[S_ALPHA] = a;
-          salpha = a;
-          cnt[C_SPMV] = 0;
-          __threadfence();
-          atomicAdd(&cnt[C_GEN], 1u);
-        }
-      } else if (tid == 0) {
-        while (ld_acquire(&cnt[C_GEN]) == sgen) __nanosleep(32);
-        salpha = __ldcg(scal + S_ALPHA);
-      }
-      if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // q for the TMA below
-    }
-    __syncthreads();
-  }
-  TRACE(3);
-  // ---------------- phase 2: first-tier up for this CTA's groups
-  const double alpha = salpha;
-  double rr = 0.0, gd = 0.0;
-  uint32_t ph = 0;
-  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
-    if (tid == 0) {
-      if (gi != (int)blockIdx.x) stage(gi, true, true);
-      else if (sn0 > 0) skq = stage_window(&bar, sm + td.o_uq, q, 8, sa0, (int64_t)sa0 + sn0);
-      mbar_arrive(&bar);
-    }
-    mbar_wait(&bar, ph);
-    ph ^= 1;
-    __syncthreads();  // the staged offsets (sa0, sk*) are visible
-    const int a1 = sa0, n1 = sn0;
-    double* rs = reinterpret_cast<double*>(sm + td.o_uy0) + skr;
-    const double* qs = reinterpret_cast<const double*>(sm + td.o_uq) + skq;
-    const double* hs = reinterpret_cast<const double*>(sm + td.o_uh) + skh;
-    for (int i = tid; i < n1; i += TPB) {
-      const double ri = rs[i] - alpha * qs[i];
-      rs[i] = ri;
-      r[a1 + i] = ri;
-      rr += ri * ri;
-      gd += hs[i] * ri;
-    }
-    if (nl > 1) {
-      __syncthreads();
-      const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
-      const int np = sn1;
-      double* yp = Yg + lv.off[nl - 1] + sa1;  // level k1 = nl (k0 = 1)
-      constexpr int FG = MSP_FLAT_G;
-      const int sub = tid & (FG - 1);
-      for (int base = 0; base < np; base += TPB / FG) {
-        const int i = base + tid / FG;
-        double ya = 0.0, yb = 0.0;
-        if (i < np) {
-          const int c0 = f[i] - a1, c1 = f[i + 1] - a1;
-          int c = c0 + sub;
-          for (; c + FG < c1; c += 2 * FG) { ya += rs[c]; yb += rs[c + FG]; }
-          if (c < c1) ya += rs[c];
-        }
-        double y = ya + yb;
-#pragma unroll
-        for (int o = FG / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-        if (sub == 0 && i < np) yp[i] = y;
-      }
-    }
-    __syncthreads();  // before the next group's TMA overwrites the windows
-  }
-  TRACE(4);
-  pdl_trigger();
-  const double2 v = block_sum2<TPB>(make_double2(rr, gd));
-  if (tid < 32) {
-    if (tid == 0) { part_rr[blockIdx.x] = v.x; part_gd[blockIdx.x] = v.y; }
-    if (warp_last_block(&cnt[C_UPD])) {
-      const double tot = warp_sum_partials(part_rr, gridDim.x);
-      const double tgd = warp_sum_partials(part_gd, gridDim.x);
-      if (tid == 0) {
-        scal[S_GD] = tgd;
-        finish_rr(tot, scal, cnt, M_ITER);
-        cnt[C_UPD] = 0;
-      }
-    }
-  }
   TRACE_END();
 }
 
@@ -2328,8 +2066,7 @@ void dist_after_tier1_down(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
 }
 
 void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P,
-                DistCtx* dc = nullptr, unsigned fused = 0) {
-  // fused != 0: the first tier's up kernel ran inside k_spmv_up (grid `fused`)
+                DistCtx* dc = nullptr) {
   const int mbase = mode & 15;
   double* part_rr = h.red.p;                  // [cap/4]
   double* part_rz = h.red.p + h.red_cap / 4;
@@ -2337,10 +2074,9 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
   unsigned* cnt = h.counters.p;
   double* scal = h.scal.p;
   const int nt = (int)h.tiers.size();
-  const int npart_up =
-      fused ? (int)fused : (int)((h.tiers[0].ntiles + h.tiers[0].up_group - 1) / h.tiers[0].up_group);
+  const int npart_up = (int)((h.tiers[0].ntiles + h.tiers[0].up_group - 1) / h.tiers[0].up_group);
   // ---- up
-  for (int i = fused ? 1 : 0; i < nt; ++i) {
+  for (int i = 0; i < nt; ++i) {
     auto& T = h.tiers[i];
     P.begin();
     if (T.generic) {
@@ -2438,35 +2174,6 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
   ++h.launches;
 }
 
-// the k_spmv_up instance for this graph's SELL layout (as launch_spmv_pairs)
-const void* spmv_up_kernel(const Handle& h) {
-  if (h.sell_uniform && h.sell_maxw == 4) return (const void*)k_spmv_up<4, true>;
-  if (h.sell_uniform && h.sell_maxw == 6) return (const void*)k_spmv_up<6, true>;
-  if (h.sell_uniform && h.sell_maxw == 8) return (const void*)k_spmv_up<8, true>;
-  if (h.sell_maxw <= 4) return (const void*)k_spmv_up<4, false>;
-  if (h.sell_maxw <= 8) return (const void*)k_spmv_up<8, false>;
-  return (const void*)k_spmv_up<16, false>;
-}
-
-void launch_spmv_up(Handle& h, const Lv& lv, const double* zp_in, double* zp_out, double* x, cudaStream_t st) {
-  auto& T = h.tiers[0];
-  auto go = [&](auto kern) {
-    launch(kern, h.fuse_grid, TPB, T.smem_up, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
-           (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
-           (const double*)h.w1.p, reinterpret_cast<const double2*>(zp_in), zp_out, h.vq.p, x, h.red.p, lv, T.desc,
-           (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, h.vr.p, (const double*)h.Hvec.p, h.Y.p,
-           h.red.p, h.red.p + h.red_cap / 2, h.scal.p, h.counters.p);
-  };
-  if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_up<4, true>);
-  else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_up<6, true>);
-  else if (h.sell_uniform && h.sell_maxw == 8) go(k_spmv_up<8, true>);
-  else if (h.sell_maxw <= 4) go(k_spmv_up<4, false>);
-  else if (h.sell_maxw <= 8) go(k_spmv_up<8, false>);
-  else go(k_spmv_up<16, false>);
-  ++h.launches;
-}
-
 // SpMV of the MSP iteration on interleaved (z, p) pairs (M_ZS2)
 void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
   auto go = [&](auto kern) {
@@ -2496,13 +2203,6 @@ void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t
     double* zin = h.pparity ? h.zp2.p : h.zp1.p;
     double* zout = h.pparity ? h.zp1.p : h.zp2.p;
     h.pparity ^= 1;
-    if (h.fuse_grid) {
-      P.begin();
-      launch_spmv_up(h, lv, zin, zout, x, st);
-      P.end(PC_SPMV);
-      msp_sweeps(h, lv, h.vq.p, h.vr.p, zout, st, M_ITER | M_ZS2, P, nullptr, h.fuse_grid);
-      return;
-    }
     P.begin();
     launch_spmv_pairs(h, zin, zout, h.vq.p, x, st);
     P.end(PC_SPMV);
@@ -2675,28 +2375,7 @@ void alloc_solve_workspace(Handle& h) {
       }
     }
   }
-  // fused SpMV + first-tier up: persistent grid no larger than the number of
-  // co-resident CTAs (its grid barrier spins)
-  h.fuse_grid = 0;
-  if (std::getenv("MSP_FUSE") && use_pairs(h) && !h.tiers.empty() && !h.tiers[0].generic &&
-      h.tiers[0].k0 == 1) {
-    const auto& T = h.tiers[0];
-    const void* f = spmv_up_kernel(h);
-    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_up));
-    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    int per_sm = 0, dev = 0, nsm = 0;
-    MSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, TPB, T.smem_up));
-    MSP_CUDA(cudaGetDevice(&dev));
-    MSP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int64_t ngroups = (T.ntiles + T.up_group - 1) / T.up_group;
-    const int64_t cap = (int64_t)per_sm * nsm;
-    // Opt-in (MSP_FUSE=1): measured slower on configs[1] (87.6 vs 85.2 us
-    // per iteration: 512 CTAs cannot spread evenly over 148 SMs in the SpMV
-    // phase), and a grid equal to the occupancy bound deadlocked (SMs whose
-    // shared-memory carveout was set by an earlier kernel cannot take their
-    // share while the resident CTAs spin), so the grid keeps a margin.
-    if (cap > 0) h.fuse_grid = (unsigned)std::min<int64_t>(ngroups, cap * 7 / 8);
-  }
+
 }
 
 void gather_to_nested(Handle& h, const double* src, double* dst, cudaStream_t st) {
