@@ -310,3 +310,30 @@ def test_two_tiers_merged_coarse():
     L = GR.laplacian_of_graph(g)
     x = out["x"].cpu().numpy()
     assert np.linalg.norm(b - L @ x) <= 2e-8 * np.linalg.norm(b)
+
+
+def test_full_size_config1_apply_R_and_pcg():
+    """configs[1] at full size (1,048,576 vertices; the bench's workload and
+    launch configuration): apply_R on the full vector against the oracle (bar
+    of test_apply_R_msp), R symmetric to 1e-12, and the PCG-MSP solve to rtol
+    1e-8 whose true residual ||b - L x|| meets the tolerance."""
+    g = G.config_graph(1)
+    s = gpu_setup(g, 0.8, 0, 0)
+    assert s.info()["ntiers"] >= 2
+    h = A.build_hierarchy(g, 0)
+    sysm = E.expand_msp_only(g, h, 0.8)
+    r = G.rhs(g.n, 0)
+    z = s.apply_R(dt(r)).cpu().numpy()
+    err = relmax(z, PR.msp(sysm)(r))
+    if err > 1e-12:
+        assert err <= max(1e-12, 50 * weight_sensitivity(sysm, r)), err
+    rng = np.random.default_rng(9)
+    u, v = rng.standard_normal(g.n), rng.standard_normal(g.n)
+    Ru = s.apply_R(dt(u)).cpu().numpy()
+    Rv = s.apply_R(dt(v)).cpu().numpy()
+    assert abs(u @ Rv - v @ Ru) <= 1e-12 * np.linalg.norm(u) * np.linalg.norm(Rv)
+    out = s.pcg_solve(dt(r), rtol=1e-8, maxit=50000)
+    assert out["converged"] == 1
+    L = GR.laplacian_of_graph(g)
+    x = out["x"].cpu().numpy()
+    assert np.linalg.norm(r - L @ x) <= 2e-8 * np.linalg.norm(r)
