@@ -177,6 +177,9 @@ struct Handle {
   DBuf<double> zp1, zp2;      // MSP path: interleaved (z_i, p_i) pairs, ping-pong
   int pparity = 0;            // which of vp / vp2 holds the current p
   cudaGraphExec_t graph = nullptr;  // captured batch of PCG iterations
+  cudaGraphExec_t pegp_graph = nullptr;  // captured batch of PEGP inner CG iterations
+  int64_t pegp_graph_launches = 0;
+  const double* pegp_graph_z = nullptr;  // the output vector the PEGP graph was captured with
   int graph_batch = 0;
   int64_t graph_launches = 0;
   cudaStream_t own_stream = nullptr;  // capture / replay stream of the graph
@@ -193,6 +196,7 @@ struct Handle {
   Handle(const Handle&) = delete;
   ~Handle() {
     if (graph) cudaGraphExecDestroy(graph);
+    if (pegp_graph) cudaGraphExecDestroy(pegp_graph);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);

@@ -251,19 +251,31 @@ __global__ void k_shift(int64_t n, double* __restrict__ a, const double* __restr
 }
 
 // CG vector updates with device scalars
+// frozen (optional): once the inner CG has converged the updates stop, so a
+// captured batch may run past convergence; its (optional) counts iterations
 __global__ void k_axpy2(int64_t n, const double* __restrict__ num, const double* __restrict__ den,
                         double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
-                        const double* __restrict__ q) {
+                        const double* __restrict__ q, const double* __restrict__ frozen = nullptr,
+                        double* __restrict__ its = nullptr) {
+  if (frozen && *frozen != 0.0) return;
+  if (its && blockIdx.x == 0 && threadIdx.x == 0) *its += 1.0;
   const double a = *num / *den;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) { x[i] += a * p[i]; r[i] -= a * q[i]; }
 }
 
 __global__ void k_pupd(int64_t n, const double* __restrict__ num, const double* __restrict__ den,
-                       const double* __restrict__ z, double* __restrict__ p) {
+                       const double* __restrict__ z, double* __restrict__ p,
+                       const double* __restrict__ frozen = nullptr) {
+  if (frozen && *frozen != 0.0) return;
   const double b = *num / *den;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = z[i] + b * p[i];
+}
+
+// the convergence test of the inner CG on the device: (r, r) <= tol^2 (b, b)
+__global__ void k_freeze(const double* __restrict__ rr, const double* __restrict__ tol2, double* __restrict__ frozen) {
+  if (*frozen == 0.0 && *rr <= *tol2) *frozen = 1.0;
 }
 
 __global__ void k_gather_canon(int64_t nk, const int32_t* __restrict__ order, int64_t off, const double* __restrict__ src,
@@ -275,7 +287,7 @@ __global__ void k_gather_canon(int64_t nk, const int32_t* __restrict__ order, in
 }
 
 struct Dots {  // device scalar slots of the PEGP inner CG
-  enum { SUMR = 0, GDOT, RHO, RZ, RZ_OLD, PQ, RR, BB, N };
+  enum { SUMR = 0, GDOT, RHO, RZ, RZ_OLD, PQ, RR, BB, TOL2, FROZEN, ITS, N };
 };
 
 }  // namespace
@@ -395,22 +407,65 @@ int solve_LH_nested(Handle& h, const double* rt_in, double* z, cudaStream_t st) 
   apply_LT_pinv_nested(h, h.er.p, h.ez.p, st);
   dot(h, nt, h.er.p, h.ez.p, d + Dots::RZ, st);
   k_copy<<<gn, TPB, 0, st>>>(nt, h.ez.p, h.ep.p);
-  int it = 0;
-  for (; it < h.pegp_maxit; ++it) {
-    apply_LH_nested(h, h.ep.p, h.eq.p, st);
-    dot(h, nt, h.ep.p, h.eq.p, d + Dots::PQ, st);
-    k_axpy2<<<gn, TPB, 0, st>>>(nt, d + Dots::RZ, d + Dots::PQ, z, h.ep.p, h.er.p, h.eq.p);
-    dot(h, nt, h.er.p, h.er.p, d + Dots::RR, st);
-    h.launches += 1;
-    if ((it & 3) == 3 || it + 1 == h.pegp_maxit) {
-      if (read_slot(h, Dots::RR, st) <= tol2) { ++it; break; }
-    }
-    apply_LT_pinv_nested(h, h.er.p, h.ez.p, st);
-    MSP_CUDA(cudaMemcpyAsync(d + Dots::RZ_OLD, d + Dots::RZ, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    dot(h, nt, h.er.p, h.ez.p, d + Dots::RZ, st);
-    k_pupd<<<gn, TPB, 0, st>>>(nt, d + Dots::RZ, d + Dots::RZ_OLD, h.ez.p, h.ep.p);
-    h.launches += 2;
+  // inner iterations in captured batches (the graph is fixed per handle: every
+  // vector is a handle buffer); the convergence test runs on the device after
+  // every iteration and freezes the updates, the host reads it per batch
+  {
+    const double init[3] = {tol2, 0.0, 0.0};  // TOL2, FROZEN, ITS
+    MSP_CUDA(cudaMemcpyAsync(d + Dots::TOL2, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
+  auto one_iteration = [&](cudaStream_t s2) {
+    apply_LH_nested(h, h.ep.p, h.eq.p, s2);
+    dot(h, nt, h.ep.p, h.eq.p, d + Dots::PQ, s2);
+    k_axpy2<<<gn, TPB, 0, s2>>>(nt, d + Dots::RZ, d + Dots::PQ, z, h.ep.p, h.er.p, h.eq.p, d + Dots::FROZEN,
+                                d + Dots::ITS);
+    dot(h, nt, h.er.p, h.er.p, d + Dots::RR, s2);
+    k_freeze<<<1, 1, 0, s2>>>(d + Dots::RR, d + Dots::TOL2, d + Dots::FROZEN);
+    apply_LT_pinv_nested(h, h.er.p, h.ez.p, s2);
+    MSP_CUDA(cudaMemcpyAsync(d + Dots::RZ_OLD, d + Dots::RZ, sizeof(double), cudaMemcpyDeviceToDevice, s2));
+    dot(h, nt, h.er.p, h.ez.p, d + Dots::RZ, s2);
+    k_pupd<<<gn, TPB, 0, s2>>>(nt, d + Dots::RZ, d + Dots::RZ_OLD, h.ez.p, h.ep.p, d + Dots::FROZEN);
+    h.launches += 4;
+  };
+  const int kb = 8;  // iterations per captured batch
+  const bool use_graph = std::getenv("MSP_NO_GRAPH") == nullptr;
+  if (use_graph && !h.own_stream) {
+    MSP_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
+    MSP_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+    MSP_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+  }
+  int it = 0;
+  for (int done_b = 0; it < h.pegp_maxit && !done_b; it += kb) {
+    if (use_graph) {
+      cudaStream_t gs = h.own_stream;
+      MSP_CUDA(cudaEventRecord(h.ev_fork, st));
+      MSP_CUDA(cudaStreamWaitEvent(gs, h.ev_fork, 0));
+      if (h.pegp_graph && h.pegp_graph_z != z) {
+        cudaGraphExecDestroy(h.pegp_graph);
+        h.pegp_graph = nullptr;
+      }
+      if (!h.pegp_graph) {
+        h.pegp_graph_z = z;
+        const int64_t l0 = h.launches;
+        cudaGraph_t g;
+        MSP_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        for (int b = 0; b < kb; ++b) one_iteration(gs);
+        MSP_CUDA(cudaStreamEndCapture(gs, &g));
+        MSP_CUDA(cudaGraphInstantiate(&h.pegp_graph, g, 0));
+        cudaGraphDestroy(g);
+        h.pegp_graph_launches = h.launches - l0;
+      } else {
+        h.launches += h.pegp_graph_launches;
+      }
+      MSP_CUDA(cudaGraphLaunch(h.pegp_graph, gs));
+      MSP_CUDA(cudaEventRecord(h.ev_join, gs));
+      MSP_CUDA(cudaStreamWaitEvent(st, h.ev_join, 0));
+    } else {
+      for (int b = 0; b < kb; ++b) one_iteration(st);
+    }
+    done_b = read_slot(h, Dots::FROZEN, st) != 0.0;
+  }
+  it = (int)read_slot(h, Dots::ITS, st);
   MSP_LAUNCH_CHECK();
   h.pegp_last_inner = it;
   return it;
