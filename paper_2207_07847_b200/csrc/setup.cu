@@ -1299,7 +1299,7 @@ void build_schedule(Handle& h, cudaStream_t st) {
       // the up kernel takes `up_group` consecutive tiles per CTA (its level-1
       // pass is a plain stream; more work per CTA amortises the fixed cost)
       {
-        int G = (k0_ == 1) ? 4 : 1;
+        int G = (k0_ == 1) ? 8 : 1;  // 1 / 2 / 4 / 6 / 8 / 16 measured on configs[1..3]: 8 best
         if (const char* e = std::getenv("MSP_UP_GROUP")) G = (k0_ == 1) ? std::max(1, std::atoi(e)) : 1;
         int64_t c0 = 0, c1 = 0;
         for (int64_t j = 0; j < t.ntiles; j += G) {
