@@ -47,6 +47,7 @@ struct TierDesc {
   int o_uf, o_uy0, o_uq, o_uh, smem_up;
   int up_group;    // tiles per CTA of the up kernel (1 when distributed)
   int nseg;        // static (constant-data) segments per tile of the down kernel
+  int tpc;         // tiles per CTA of the down kernel (first tier; one after another)
 };
 
 // One static TMA segment of a tile of the down kernel, precomputed at setup

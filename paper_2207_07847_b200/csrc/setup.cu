@@ -1255,6 +1255,7 @@ void build_schedule(Handle& h, cudaStream_t st) {
       }
       const bool top = (k1_ == h.Kc) && gemv_ok;
       t.desc = tier_layout(k0_, nl, t.ntiles, cap, caplo, top ? h.lv[h.Kc - 1].n : 0);
+      t.desc.tpc = 1;  // first tier: set in alloc_solve_workspace (needs the occupancy)
       // static TMA segments of every tile of the down kernel (sched.cuh)
       {
         const int S = 3 * (nl - 1) + (k0_ > 1 ? 1 : 0);

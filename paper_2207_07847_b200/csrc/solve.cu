@@ -1211,7 +1211,10 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   __shared__ LvlPtr tb[MAXT];
   __shared__ CoarseState C;
   __shared__ double sgd;
-  const int tile = blockIdx.x + tile0, nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
+  // first tier (not distributed): tpc consecutive tiles per CTA, one after
+  // another (the block reduction and ticket once per CTA)
+  const int tpc = (FIRST && !COARSE && !(mode_in & M_DIST) && td.tpc > 1) ? td.tpc : 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   if ((COARSE ? (MSP_EARLY & 4) : FIRST ? (MSP_EARLY & 8) : (MSP_EARLY & 4)) != 0) pdl_trigger();
@@ -1221,6 +1224,11 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     mbar_init(&bar, 1);
     if (COARSE) mbar_init(&C.bar, 1);
   }
+  double rz = 0.0;
+  #pragma unroll 1
+  for (int tt = 0; tt < tpc; ++tt) {
+  const int tile = (int)blockIdx.x * tpc + tt + tile0;
+  if (tile >= td.ntiles) break;  // uniform
   if (tid < nl) {
     const int a = tstart[tid * nt1 + tile];
     sa[tid] = a;
@@ -1322,7 +1330,7 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     mbar_arrive(&bar);
     if (COARSE) mbar_arrive(&C.bar);
   }
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar, (uint32_t)(tt & 1));
   TRACE(3);
   PHASE(2);
   // per-level pointer table (one thread per level), so every phase starts
@@ -1465,7 +1473,6 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   // ---- down: levels k1-1 .. k0+1 in shared memory, then level k0 out
   const double rho = srho;
   const double negmu = lv.negmu;
-  double rz = 0.0;
   for (int t = nl - 2; t >= 1; --t) {  // child level k = k0+t, parent level k+1
     __syncthreads();
     TRACE(6 + t);
@@ -1522,13 +1529,15 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
             [&](int p, double z, double w) { zg[p] = z; wg[p] = w; });
     }
   }
+  if (tt + 1 < tpc) __syncthreads();  // the next tile's copies overwrite shared memory
+  }  // tiles of this CTA
   TRACE(5);
   PHASE(5);
   pdl_trigger();
   if (FIRST) {
     rz = block_sum<NT>(rz);
     if (tid < 32) {  // only warp 0 waits on the ticket
-      if (tid == 0) part[tile] = rz;
+      if (tid == 0) part[blockIdx.x + tile0] = rz;
       if (mode != M_APPLY && warp_last_block(&cnt[C_DOWN])) {
         const double tot = warp_sum_partials(part + tile0, gridDim.x);
         if (tid == 0) {
@@ -2137,7 +2146,8 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : T.ntiles), TT, T.smem_down, st, lv,
+        launch(k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.desc.tpc - 1) / T.desc.tpc),
+               TT, T.smem_down, st, lv,
                T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
@@ -2347,6 +2357,21 @@ void alloc_solve_workspace(Handle& h) {
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   for (auto f : {(const void*)k_tile_down<true>, (const void*)k_tile_down<false>})
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  // first tier down: tiles per CTA -- about one wave of resident CTAs, at most
+  // 8 tiles each (configs[1..3]: 2 / 8 / 8 measured best or within 0.5 %)
+  for (auto& T : h.tiers) {
+    if (T.generic || T.k0 != 1 || T.k1 == T.k0) continue;
+    int per_sm = 0, dev = 0, nsm = 0;
+    MSP_CUDA(cudaFuncSetAttribute((const void*)k_tile_down<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    MSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_tile_down<true>, TT,
+                                                           T.smem_down));
+    MSP_CUDA(cudaGetDevice(&dev));
+    MSP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t slots = std::max<int64_t>(1, (int64_t)per_sm * nsm);
+    int tpc = (int)std::min<int64_t>(8, (T.ntiles + slots - 1) / slots);
+    if (const char* e = std::getenv("MSP_DOWN_TPC")) tpc = std::max(1, std::atoi(e));
+    T.desc.tpc = std::max(1, tpc);
+  }
   for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>, (const void*)k_tile_down<true>,
                  (const void*)k_tile_down<false>})
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
