@@ -1225,20 +1225,27 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     if (COARSE) mbar_init(&C.bar, 1);
   }
   double rz = 0.0;
+  // the next tile's ranges and segment descriptors are loaded into registers
+  // while the current one computes
+  int pa = 0, pb = 0;
+  int4 psd = make_int4(0, 0, 0, 0);
+  auto load_idx = [&](int tl) {
+    if (tid < nl) { pa = tstart[tid * nt1 + tl]; pb = tstart[tid * nt1 + tl + 1]; }
+    if (tid < td.nseg) psd = __ldg(segs + (int64_t)tl * td.nseg + tid);
+  };
+  load_idx((int)blockIdx.x * tpc + tile0);
   #pragma unroll 1
   for (int tt = 0; tt < tpc; ++tt) {
   const int tile = (int)blockIdx.x * tpc + tt + tile0;
   if (tile >= td.ntiles) break;  // uniform
   if (tid < nl) {
-    const int a = tstart[tid * nt1 + tile];
-    sa[tid] = a;
-    sn[tid] = tstart[tid * nt1 + tile + 1] - a;
+    sa[tid] = pa;
+    sn[tid] = pb - pa;
   }
   // static segments (child pointers, factors, leftover coefficients, N_k0),
   // one per thread from the tile's precomputed descriptors; after the grid
   // dependency: y_k0, z, w
-  int4 sd = make_int4(0, 0, 0, 0);
-  if (tid < td.nseg) sd = __ldg(segs + (int64_t)tile * td.nseg + tid);
+  const int4 sd = psd;
   __syncthreads();
   if (tid < td.nseg) {
     const int kind = sd.x & 3, t = (sd.x >> 2) & 63, dst = sd.x >> 8;
@@ -1331,6 +1338,7 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
     if (COARSE) mbar_arrive(&C.bar);
   }
   mbar_wait(&bar, (uint32_t)(tt & 1));
+  if (tt + 1 < tpc && tile + 1 < td.ntiles) load_idx(tile + 1);
   TRACE(3);
   PHASE(2);
   // per-level pointer table (one thread per level), so every phase starts
