@@ -48,7 +48,7 @@ constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
 #define MSP_SPMV_LB 4  // min CTAs/SM of the pipelined SpMV (register budget)
 #endif
 #ifndef MSP_EARLY
-#define MSP_EARLY 1  // measured: 1 (tier-2 up triggers at its start) -1.6 us; other bits neutral or worse
+#define MSP_EARLY 17  // measured: bit 1 (tier-2 up) -1.6 us, bit 16 (SpMV) -0.5 us; bits 2, 4, 8 neutral or worse
 #endif
 #ifndef MSP_FLAT_G
 #define MSP_FLAT_G 8  // lanes per level-k1 node in the up kernels (2 / 4 / 8 / 16 / 32 measured; 8 best)
