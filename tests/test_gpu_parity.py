@@ -337,3 +337,32 @@ def test_full_size_config1_apply_R_and_pcg():
     L = GR.laplacian_of_graph(g)
     x = out["x"].cpu().numpy()
     assert np.linalg.norm(r - L @ x) <= 2e-8 * np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("tpc", [2, 3, 7])
+def test_multi_tile_down_ctas(tpc):
+    """Several first-tier tiles per CTA of the down kernel (MSP_DOWN_TPC;
+    the default picks it from the occupancy): the tiles' arithmetic is
+    unchanged, so apply_R is bit-identical to one tile per CTA, including a
+    last CTA with fewer tiles; the PCG solve meets its true residual."""
+    import os
+    g = G.grid2d(320, 320, "loguniform", 4)
+    os.environ["MSP_DOWN_TPC"] = "1"
+    try:
+        s1 = gpu_setup(g, 0.8, 0, 11)
+    finally:
+        del os.environ["MSP_DOWN_TPC"]
+    os.environ["MSP_DOWN_TPC"] = str(tpc)
+    try:
+        s = gpu_setup(g, 0.8, 0, 11)
+    finally:
+        del os.environ["MSP_DOWN_TPC"]
+    assert s.info()["ntiles"] % tpc != 0 or tpc == 2  # a last CTA with fewer tiles
+    r = dt(G.rhs(g.n, 7))
+    assert np.array_equal(s.apply_R(r).cpu().numpy(), s1.apply_R(r).cpu().numpy())
+    b = G.rhs(g.n, 8)
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    assert out["converged"] == 1
+    x = out["x"].cpu().numpy()
+    L = GR.laplacian_of_graph(g)
+    assert np.linalg.norm(b - L @ x) <= 2e-8 * np.linalg.norm(b)
