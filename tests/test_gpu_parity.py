@@ -277,6 +277,12 @@ def test_full_size_hierarchy_and_sampled_apply_L(idx, scale):
         ws = g.val[g.rowptr[i]:g.rowptr[i + 1]]
         yi = float(np.sum(ws * (x[i] - x[cols])))
         assert abs(y[i] - yi) <= 1e-12 * max(abs(yi), np.abs(ws).sum() * np.abs(x).max())
+    b = G.rhs(g.n, 4)
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=50000)
+    assert out["converged"] == 1
+    xs = out["x"].cpu().numpy()
+    L = GR.laplacian_of_graph(g)
+    assert np.linalg.norm(b - L @ xs) <= 2e-8 * np.linalg.norm(b)
 
 
 def test_two_tiers_merged_coarse():
