@@ -40,7 +40,11 @@ constexpr int TPB = 256;      // SpMV and per-node kernels
 #ifndef MSP_TT
 #define MSP_TT 128
 #endif
-constexpr int TT = MSP_TT;    // tile kernels (threads per CTA)
+constexpr int TT = MSP_TT;
+#ifndef MSP_UT
+#define MSP_UT 256  // 128 / 256 / 512 measured on configs[1]: 65.2 / 64.2 / 64.7 us per iteration
+#endif
+constexpr int UT = MSP_UT;   // tile up kernels (threads per CTA)    // tile kernels (threads per CTA)
 #ifndef MSP_PF_DIST
 #define MSP_PF_DIST 1
 #endif
@@ -719,7 +723,7 @@ __global__ void k_x_final_pairs(int64_t n, double* __restrict__ x, const double*
 #undef TRACE_KID
 #define TRACE_KID (FIRST ? 4 : 5)
 template <bool FIRST>
-__global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
+__global__ void __launch_bounds__(UT) k_tile_up(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
                                                 const int32_t* __restrict__ tstart, const int32_t* __restrict__ firstk0,
                                                 const double* __restrict__ q, double* __restrict__ r,
                                                 const double* __restrict__ H, double* __restrict__ Yg,
@@ -801,7 +805,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     const int* f = reinterpret_cast<const int*>(sm + td.o_uf) + skf;
     double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
     #pragma unroll 1
-    for (int base = 0; base < np; base += TT / FG) {  // block-uniform trip count
+    for (int base = 0; base < np; base += UT / FG) {  // block-uniform trip count
       const int i = base + tid / FG;
       double y = 0.0;
       if (i < np) {
@@ -829,7 +833,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     double* rs = y0 + skr;
     const double* qs = reinterpret_cast<const double*>(sm + td.o_uq) + skq;
     const double* hs = reinterpret_cast<const double*>(sm + td.o_uh) + skh;
-    for (int i = tid; i < n1; i += TT) {
+    for (int i = tid; i < n1; i += UT) {
       double ri = rs[i];
       if (mode == M_ITER) {
         ri -= alpha * qs[i];
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
     double* yp = Yg + lv.off[k0 + nl - 2] + sa1;
     // FG lanes per level-k1 node, two partial sums per lane, then a
     // butterfly over the group (fixed order)
-    for (int base = 0; base < np; base += TT / FG) {  // block-uniform trip count
+    for (int base = 0; base < np; base += UT / FG) {  // block-uniform trip count
       const int i = base + tid / FG;
       double ya = 0.0, yb = 0.0;
       if (i < np) {
@@ -865,7 +869,7 @@ __global__ void __launch_bounds__(TT) k_tile_up(const __grid_constant__ Lv lv, c
   PHASE(4);
   pdl_trigger();
   if (FIRST) {
-    const double2 v = block_sum2<TT>(make_double2(rr, gd));
+    const double2 v = block_sum2<UT>(make_double2(rr, gd));
     TRACE(6);
     PHASE(5);
     if (tid < 32) {  // only warp 0 waits on the ticket
@@ -2105,12 +2109,12 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       P.end(PC_MID_UP);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), TT,
+        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), UT,
                T.smem_up, st, lv,
                T.desc, (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p,
                h.Y.p, part_rr, part_gd, scal, cnt, mode | (dc ? M_DIST : 0), (int)(dc ? dc->tile0 : 0));
       else
-        launch(k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), TT, T.smem_up, st, lv, T.desc,
+        launch(k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), UT, T.smem_up, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
                part_rr, part_gd, scal, cnt, mode, 0);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
