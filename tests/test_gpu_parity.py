@@ -283,6 +283,12 @@ def test_full_size_hierarchy_and_sampled_apply_L(idx, scale):
     xs = out["x"].cpu().numpy()
     L = GR.laplacian_of_graph(g)
     assert np.linalg.norm(b - L @ xs) <= 2e-8 * np.linalg.norm(b)
+    if idx in (2, 3):  # apply_R against the oracle at this size (bar of test_apply_R_msp)
+        sysm = E.expand_msp_only(g, h, 0.8)
+        z = s.apply_R(dt(b)).cpu().numpy()
+        err = relmax(z, PR.msp(sysm)(b))
+        if err > 1e-12:
+            assert err <= max(1e-12, 50 * weight_sensitivity(sysm, b)), err
 
 
 def test_two_tiers_merged_coarse():
