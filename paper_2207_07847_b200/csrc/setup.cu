@@ -1168,7 +1168,7 @@ void build_schedule(Handle& h, cudaStream_t st) {
     double c = 0.0, pw = 1.0;
     for (int k = 1; k <= L; ++k) { c += pw; pw *= -h.mu; h.ck[k] = c; }
   }
-  int64_t T = 512, SUB = 256, CMAX = 1024;  // CMAX: measured best over configs[1..3]
+  int64_t T = 512, SUB = 256, CMAX = 512;   // CMAX: measured best over configs[1..3]
   if (const char* e = std::getenv("MSP_TILE_T")) T = std::max<int64_t>(16, std::atoll(e));
   SUB = T / 2;
   if (const char* e = std::getenv("MSP_TILE_SUB")) SUB = std::max<int64_t>(2, std::atoll(e));
