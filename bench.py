@@ -302,6 +302,10 @@ def main():
         e_iters.append(r2["iterations"])
     torch.cuda.synchronize()
     te = time.perf_counter() - te
+    if world > 1:  # slowest rank
+        t = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
     e2e_value = world * g.nnz_laplacian * sum(e_iters) / te
 
     # ---- profiled replay of one step: per-kernel device time (CUDA events)
