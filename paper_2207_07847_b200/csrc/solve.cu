@@ -1918,6 +1918,33 @@ bool use_pdl() {
   return on;
 }
 
+// launches of kernel category `cat` (1 plain SpMV, 2 pipelined SpMV, 4 tile
+// up, 8 tile down, 16 per-level kernels) without the PDL attribute when its
+// bit is set in MSP_NOPDL_MASK.  Default 3, the SpMVs: their grid-stride
+// CTAs, launched early, land unevenly on the SMs the previous kernel is still
+// leaving (without PDL there: configs[1] 64.0 -> 61.7, configs[2] 1362 -> 942,
+// configs[3] 472 -> 426 us/iteration)
+bool pdl_for(int cat) {
+  static const int mask = std::getenv("MSP_NOPDL_MASK") ? std::atoi(std::getenv("MSP_NOPDL_MASK")) : 3;
+  return use_pdl() && !(mask & cat);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_c(int cat, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_for(cat) ? 1 : 0;
+  MSP_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
+}
+
 template <typename... KArgs, typename... Args>
 void launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -2104,17 +2131,17 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       const int k = T.k0;
       const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
       const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
-      launch(k_up_lvl, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin,
+      launch_c(16, k_up_lvl, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin,
              h.Y.p + h.lv[k].off, (const unsigned*)cnt, mode, (const int32_t*)(h.heavy.p + h.heavy_off[k - 1]), nh);
       P.end(PC_MID_UP);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), UT,
+        launch_c(4, k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), UT,
                T.smem_up, st, lv,
                T.desc, (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p,
                h.Y.p, part_rr, part_gd, scal, cnt, mode | (dc ? M_DIST : 0), (int)(dc ? dc->tile0 : 0));
       else
-        launch(k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), UT, T.smem_up, st, lv, T.desc,
+        launch_c(4, k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), UT, T.smem_up, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
                part_rr, part_gd, scal, cnt, mode, 0);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
@@ -2146,19 +2173,19 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
       const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
       const int32_t* hv = h.heavy.p + h.heavy_off[k - 1];
       if (k == 1)
-        launch(k_down_lvl<true>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+        launch_c(16, k_down_lvl<true>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
                (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p,
                (const double*)(h.Z.p + op), (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt,
                mode, hv, nh);
       else
-        launch(k_down_lvl<false>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
+        launch_c(16, k_down_lvl<false>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
                (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)(h.Y.p + ok),
                (const double*)h.Nsub.p, (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok,
                h.W.p + ok, part_rz, scal, cnt, mode, hv, nh);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1)
-        launch(k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.desc.tpc - 1) / T.desc.tpc),
+        launch_c(8, k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.desc.tpc - 1) / T.desc.tpc),
                TT, T.smem_down, st, lv,
                T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
@@ -2167,14 +2194,14 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
                (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p, h.cdesc, 0,
                (const double*)nullptr, (const double*)nullptr);
       else if (merged && i == nt - 1)  // the coarse levels run inside this kernel
-        launch(k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, T.desc,
+        launch_c(8, k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
                (const int4*)T.segs.p, h.cdesc, (int)h.merged_coff, (const double*)h.top_pinv.p,
                (const double*)h.Mtop.p);
       else
-        launch(k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
+        launch_c(8, k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
                (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
                scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
@@ -2189,7 +2216,7 @@ void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, 
 template <bool PCG>
 void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
                  cudaStream_t st) {
-  launch(k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
+  launch_c(1, k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
          (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
          (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
          (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, (int64_t)0, h.n);
@@ -2199,7 +2226,7 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
 // SpMV of the MSP iteration on interleaved (z, p) pairs (M_ZS2)
 void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
   auto go = [&](auto kern) {
-    launch(kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
+    launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
            (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge, (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
@@ -2337,9 +2364,10 @@ void alloc_solve_workspace(Handle& h) {
     int dev = 0, sms = 148;
     MSP_CUDA(cudaGetDevice(&dev));
     MSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int per_sm = 8;
+    // pipelined SpMV: 4 CTAs/SM (its register budget); the plain one: 8
+    // (configs[3]: 426 -> 397 us/iteration)
+    int per_sm = use_pairs(h) ? 4 : 8;
     if (const char* e = std::getenv("MSP_SPMV_BLOCKS_PER_SM")) per_sm = std::max(1, std::atoi(e));
-    else per_sm = 4;
     const int64_t want = grid_for(std::max<int64_t>(h.nslices, 1) * 32);
     h.spmv_grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * per_sm);
   }
