@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
   if ((MSP_EARLY & 16) != 0) pdl_trigger();
   TRACE(0);
-#ifndef MSP_NO_PF_PRE
+#ifdef MSP_SPMV_PF_PRE  // off since the SpMV launches without PDL (configs[1] 61.7 -> 61.4 us/iteration)
   if (UNIF && (threadIdx.x & 31) == 0) {  // constant streams of the first slices, before the dependency
     const int64_t w0 = (blockIdx.x * (int64_t)TPB + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * TPB) >> 5;
     for (int64_t sp = w0; sp < nslices && sp <= w0 + nw; sp += nw) {
