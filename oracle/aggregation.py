@@ -90,7 +90,8 @@ def coarsen(lv: Level, agg: np.ndarray, nc: int) -> Level:
     return Level(nc, crowptr, ccol[:cnnz].copy(), cw[:cnnz].copy())
 
 
-def build_hierarchy(g, seed: int = 0, max_levels: int = 0, orders=None) -> Hierarchy:
+def build_hierarchy(g, seed: int = 0, max_levels: int = 0, orders=None,
+                    order: str = "random") -> Hierarchy:
     """Repeated MWM coarsening (§2.2 l.59: "We then continue to
     aggregate nodes until the desired level is achieved").
 
@@ -99,7 +100,12 @@ def build_hierarchy(g, seed: int = 0, max_levels: int = 0, orders=None) -> Hiera
     level)").  Reading R5: a level is aggregated only while it has more than
     two nodes, and an aggregation that would leave fewer than two aggregates
     is not taken (the top level keeps >= 2 nodes so H~ stays connected).
-    ``orders`` optionally forces the visit order per level (tests)."""
+    ``orders`` optionally forces the visit order per level (tests).
+    ``order="natural"`` visits every level in vertex-index order: the order
+    that reproduces PAPER.md Tables 1-3 (R1); the default
+    ``"random"`` is reading R1's counter-based key."""
+    if order not in ("random", "natural"):
+        raise ValueError(order)
     h = Hierarchy(seed=seed)
     h.levels.append(Level(g.n, np.ascontiguousarray(g.rowptr, dtype=np.int64),
                           np.ascontiguousarray(g.col, dtype=np.int32),
@@ -111,8 +117,10 @@ def build_hierarchy(g, seed: int = 0, max_levels: int = 0, orders=None) -> Hiera
         lv = h.levels[-1]
         if lv.n <= 2:
             break
-        order = None if orders is None else orders[k - 1]
-        mate, agg, nc = mwm(lv, seed, k, order)
+        vo = None if orders is None else orders[k - 1]
+        if vo is None and order == "natural":
+            vo = np.arange(lv.n, dtype=np.int64)
+        mate, agg, nc = mwm(lv, seed, k, vo)
         if nc < 2:
             break
         h.mates.append(mate)
