@@ -40,6 +40,10 @@ int msp_partition_plan(int64_t n, const int32_t* rowptr, const int32_t* col, int
   tb[world] = ntiles;
   for (int r = 1; r < world; ++r) tb[r] = std::max(tb[r - 1], lower_tile(tile_rows, ntiles, (n * r) / world));
   for (int r = 0; r <= world; ++r) rb[r] = tile_rows[tb[r]];
+  // every rank must own at least one tile: the check depends only on the
+  // shared inputs, so all ranks fail together, before any collective
+  for (int r = 0; r < world; ++r)
+    if (tb[r + 1] <= tb[r]) return MSP_ERR_UNSUPPORTED;
   const int64_t r0 = rb[rank], r1 = rb[rank + 1];
   range[0] = r0;
   range[1] = r1;

@@ -34,6 +34,12 @@ void set_error(const std::string& m);
 
 #define MSP_LAUNCH_CHECK() MSP_CUDA(cudaGetLastError())
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per kernel and process-wide:
+// raise it to the largest request any handle has made, never lower it (a
+// second, smaller handle must not break launches of a larger one).  The
+// occupancy of a launch depends on the bytes it passes, not on this cap.
+void raise_smem_limit(const void* func, size_t bytes);
+
 // ---------------------------------------------------------------- device buffer
 template <typename T>
 struct DBuf {

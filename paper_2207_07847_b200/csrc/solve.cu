@@ -29,6 +29,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -2334,8 +2336,7 @@ void build_top_map(Handle& h, cudaStream_t st) {
   C.alloc(2 * nj * (nj + 1) + 8);
   h.Mtop.alloc(2 * nj * (nj + 1) + 8);
   k_unit_rows<<<grid_for((nj + 1) * nj), TPB, 0, st>>>(nj, E.p);
-  MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)std::max<size_t>(h.coarse_smem, cdj.smem)));
+  raise_smem_limit((const void*)k_coarse, std::max<size_t>(h.coarse_smem, cdj.smem));
   launch(k_coarse, (unsigned)(nj + 1), CT, (size_t)cdj.smem, st, lvj, cdj, (const int32_t*)h.cptr.p,
          (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
          (const double*)E.p, C.p, C.p, (double*)nullptr, (const double*)nullptr, 0, h.scal.p, h.counters.p,
@@ -2348,6 +2349,18 @@ void build_top_map(Handle& h, cudaStream_t st) {
   h.cdesc.o_mtop = (int)((h.cdesc.smem + 15) & ~15);
   h.cdesc.smem = (int)((h.cdesc.o_mtop + (2 * nj * (nj + 1) + 2) * 8 + 15) & ~(int64_t)15);
   h.coarse_smem = h.cdesc.smem;
+}
+
+void raise_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;  // per device and kernel
+  int dev = 0;
+  MSP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[{dev, func}];
+  if (bytes <= c) return;
+  MSP_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
 }
 
 void release_graph(Handle& h) {
@@ -2394,9 +2407,9 @@ void alloc_solve_workspace(Handle& h) {
   size_t up = 0, down = 0;
   for (auto& T : h.tiers) { up = std::max(up, T.smem_up); down = std::max(down, T.smem_down); }
   for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>})
-    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+    raise_smem_limit(f, up);
   for (auto f : {(const void*)k_tile_down<true>, (const void*)k_tile_down<false>})
-    MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+    raise_smem_limit(f, down);
   // first tier down: tiles per CTA -- about one wave of resident CTAs, at most
   // 8 tiles each (configs[1..3]: 2 / 8 / 8 measured best or within 0.5 %)
   for (auto& T : h.tiers) {
@@ -2415,8 +2428,7 @@ void alloc_solve_workspace(Handle& h) {
   for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>, (const void*)k_tile_down<true>,
                  (const void*)k_tile_down<false>})
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  MSP_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)h.coarse_smem));
+  raise_smem_limit((const void*)k_coarse, h.coarse_smem);
   // merged last-tier down + coarse kernel (tier k1 == Kc, small top)
   h.merged_coff = 0;
   h.merged_smem = 0;
@@ -2429,8 +2441,7 @@ void alloc_solve_workspace(Handle& h) {
         const size_t coff = (T.smem_down + 15) & ~(size_t)15;
         const size_t tot = coff + h.coarse_smem;
         if (tot <= 220 * 1024) {
-          MSP_CUDA(cudaFuncSetAttribute((const void*)k_tile_down<false, true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tot));
+          raise_smem_limit((const void*)k_tile_down<false, true>, tot);
           h.merged_coff = std::max<size_t>(coff, 16);
           h.merged_smem = h.merged_coff + h.coarse_smem;
           // coarse levels on 16 warps beside the tile recompute when every

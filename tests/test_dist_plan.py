@@ -120,3 +120,17 @@ def test_gloo_world2_halo_exchange_reproduces_global_spmv():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_plan_rejects_rank_without_tiles():
+    """More ranks than tiles: every rank gets MSP_ERR_UNSUPPORTED from the
+    plan (a deterministic check on shared inputs, so all ranks fail together
+    before any collective instead of one hanging)."""
+    from paper_2207_07847_b200 import _lib as L
+    from paper_2207_07847_b200.dist import partition_plan
+    g = G.grid2d(6, 5)
+    tr = tiles_of(g.n, 16)                       # 2 tiles
+    for r in range(3):
+        with pytest.raises(L.MspError) as ei:
+            partition_plan(g.n, g.rowptr, g.col, tr, 3, r)
+        assert ei.value.code == -4

@@ -119,3 +119,37 @@ def test_table5_watts_strogatz_pegp_band():
         s = E.expand(g, h, 1 / np.sqrt(n))
         it = PC.pcg(lambda x: L @ x, G.rhs_paper(n), PR.pegp(s), 1e-8, 1000).iterations
         assert abs(it - t["table5_ws_levelmax_pegp_steps"][str(n)]) <= 2, (n, it)
+
+
+@pytest.mark.parametrize("kind", ["msp", "pegp"])
+def test_refined_reference(kind):
+    """The parity reference R_X r with iterative refinement (R14):
+    the same operator as the plain apply (dense pseudo-inverse on a tiny
+    well-conditioned case to 1e-13), and on a high-contrast grid it solves
+    L_X z~ = P^T r - mean to an extended-precision residual far below what
+    the unrefined fp64 solve reaches."""
+    g, h, s = small(6, 0.8, (6, 5), "uniform1_10")
+    P = s.P()
+    LX = s.LT if kind == "msp" else s.LH
+    r = G.rhs(g.n, 2)
+    ref = PR.RefinedPreconditioner(P, LX)(r)
+    Rd = PR.dense_R(P, LX)
+    np.testing.assert_allclose(ref, Rd @ r, rtol=0, atol=1e-13 * np.abs(ref).max())
+    g = G.grid2d(40, 30, "loguniform", 8)
+    h = A.build_hierarchy(g, 1)
+    s = E.expand_msp_only(g, h, 0.8) if kind == "msp" else E.expand(g, h, 0.8)
+    LX = s.LT if kind == "msp" else s.LH
+    Rf = PR.RefinedPreconditioner(s.P(), LX)
+    r = G.rhs(g.n, 3)
+    rt = PR._ld_matvec(Rf.PT, r)
+    rt = rt - rt.mean()
+    z0 = PR.PinvSolver(LX)(np.asarray(rt, dtype=np.float64))
+    zf = Rf.inv(np.asarray(rt, dtype=np.float64)).astype(np.longdouble)
+    for _ in range(6):
+        zf = zf + Rf.inv(np.asarray(rt - PR._ld_matvec(LX, zf), dtype=np.float64))
+    res0 = np.abs(np.asarray(rt - PR._ld_matvec(LX, z0), dtype=np.float64)).max()
+    resf = np.abs(np.asarray(rt - PR._ld_matvec(LX, zf), dtype=np.float64)).max()
+    assert resf < 1e-2 * res0, (resf, res0)
+    out = Rf(r)
+    assert Rf.steps >= 1
+    np.testing.assert_allclose(out, PR.Preconditioner(s.P(), LX)(r), rtol=0, atol=1e-9 * np.abs(out).max())
