@@ -73,25 +73,56 @@ def _ld_matvec(A: sp.csr_matrix, x: np.ndarray) -> np.ndarray:
     return y
 
 
+def _ld_laplacian_apply(W: sp.csr_matrix, z: np.ndarray) -> np.ndarray:
+    """(L_X z)_i = sum_j w_ij (z_i - z_j) from the edge weights themselves, in
+    extended precision -- the Laplacian of the fp64 weights with its exact
+    diagonal (R7: "diagonal = sum of the kept weights").  An assembled fp64
+    L_X rounds that diagonal, and on high-contrast graphs (a heavy matched
+    edge beside a light parent edge) the rounding is far larger, relative to
+    the light weight, than the weights' own precision."""
+    W = sp.csr_matrix(W)
+    W.sort_indices()
+    zl = np.asarray(z, dtype=np.longdouble)
+    rows = np.repeat(np.arange(W.shape[0]), np.diff(W.indptr))
+    prod = W.data.astype(np.longdouble) * (zl[rows] - zl[W.indices])
+    y = np.zeros(W.shape[0], dtype=np.longdouble)
+    nz = np.diff(W.indptr) > 0
+    y[nz] = np.add.reduceat(prod, W.indptr[:-1][nz])
+    return y
+
+
 class RefinedPreconditioner:
     """R_X r = P(mu) L_X^+ P(mu)^T r, the same definition as
-    :class:`Preconditioner`, evaluated to (nearly) full fp64 accuracy for
-    use as the parity *reference* (R14): P^T r and P z~ in extended
-    precision, and the grounded LU solve of L_X z~ = r~ - mean(r~) followed
-    by iterative refinement -- residual in extended precision, correction by
+    :class:`Preconditioner`, evaluated to (nearly) full accuracy for the
+    given fp64 edge weights W_X, for use as the parity *reference* (DESIGN.md
+    R14): P^T r and P z~ in extended precision, and the grounded LU solve of
+    L_X z~ = r~ - mean(r~) followed by iterative refinement -- residual in
+    extended precision from the edge weights (exact diagonal), correction by
     the same LU -- until the correction stops shrinking (classical mixed-
     precision refinement, e.g. Higham, "Accuracy and Stability of Numerical
     Algorithms", ch. 12).  The result is R_X r for the given fp64 data,
-    rounded once; it differs from :class:`Preconditioner` only by that
-    solve's rounding error."""
+    rounded once."""
 
-    def __init__(self, P: sp.csr_matrix, LX: sp.spmatrix, max_steps: int = 12):
+    def __init__(self, P: sp.csr_matrix, WX: sp.spmatrix, scale=None, max_steps: int = 30):
+        from .graph import laplacian_from_weights
         self.P = sp.csr_matrix(P)
         self.PT = self.P.T.tocsr()
-        self.LX = sp.csr_matrix(LX)
-        self.inv = PinvSolver(LX)
+        self.WX = sp.csr_matrix(WX)
+        LX = laplacian_from_weights(self.WX.shape[0], self.WX)
+        # the correction solver only has to approximate L_X^+: with weights
+        # spanning mu^{2(l-1)} it factors D L_X D, D = diag(scale), whose
+        # entries are O(1) (grounded at node 0, scale 1)
+        self.d = np.ones(LX.shape[0]) if scale is None else np.asarray(scale, dtype=np.float64)
+        M = (sp.diags(self.d) @ LX @ sp.diags(self.d)).tocsc()
+        self.lu = spla.splu(M[1:, 1:].tocsc()) if M.shape[0] > 1 else None
         self.max_steps = max_steps
         self.steps = 0
+
+    def inv(self, y: np.ndarray) -> np.ndarray:
+        z = np.zeros(y.shape[0])
+        if self.lu is not None:
+            z[1:] = self.lu.solve((self.d * y)[1:])
+        return self.d * z
 
     def __call__(self, r: np.ndarray) -> np.ndarray:
         rt = _ld_matvec(self.PT, r)
@@ -100,24 +131,28 @@ class RefinedPreconditioner:
         last = np.inf
         self.steps = 0
         for _ in range(self.max_steps):
-            res = rt - _ld_matvec(self.LX, z)          # z carried in extended precision
+            res = rt - _ld_laplacian_apply(self.WX, z)   # z carried in extended precision
             c = self.inv(np.asarray(res, dtype=np.float64))
             z = z + c.astype(np.longdouble)
             self.steps += 1
             cn = float(np.abs(c).max())
-            if cn <= 1e-19 * float(np.abs(z).max()) or cn >= 0.5 * last:
+            if cn <= 1e-19 * float(np.abs(z).max()) or cn >= last:
                 break
             last = cn
         z = z - z.mean()
         return np.asarray(_ld_matvec(self.P, z), dtype=np.float64)
 
 
+def _level_scale(sys) -> np.ndarray:
+    return sys.mu ** (-(sys.level_of.astype(np.float64) - 1.0))
+
+
 def msp_refined(sys) -> RefinedPreconditioner:
-    return RefinedPreconditioner(sys.P(), sys.LT)
+    return RefinedPreconditioner(sys.P(), sys.WT, _level_scale(sys))
 
 
 def pegp_refined(sys) -> RefinedPreconditioner:
-    return RefinedPreconditioner(sys.P(), sys.LH)
+    return RefinedPreconditioner(sys.P(), sys.WH, _level_scale(sys))
 
 
 def msp(sys) -> Preconditioner:

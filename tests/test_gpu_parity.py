@@ -373,3 +373,17 @@ def test_multi_tile_down_ctas(tpc):
     x = out["x"].cpu().numpy()
     L = GR.laplacian_of_graph(g)
     assert np.linalg.norm(b - L @ x) <= 2e-8 * np.linalg.norm(b)
+
+
+def test_second_smaller_handle_keeps_first_usable():
+    """The kernels' dynamic shared-memory limit is process-wide: a second,
+    smaller setup must not lower it under the first handle."""
+    g1 = G.grid2d(320, 320, "loguniform", 4)
+    s1 = gpu_setup(g1, 0.8, 0, 11)
+    r = dt(G.rhs(g1.n, 5))
+    z_before = s1.apply_R(r).cpu().numpy()
+    s2 = gpu_setup(G.grid2d(12, 9, "uniform1_10", 1), 0.8, 0, 1)
+    s2.apply_R(dt(G.rhs(108, 1)))
+    assert np.array_equal(s1.apply_R(r).cpu().numpy(), z_before)
+    out = s1.pcg_solve(dt(G.rhs(g1.n, 6)), rtol=1e-8, maxit=20000)
+    assert out["converged"] == 1

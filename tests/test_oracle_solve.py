@@ -9,6 +9,7 @@ exact natural-order pins are in test_oracle_paper_tables.py).
 """
 import numpy as np
 import pytest
+import scipy.sparse as sp
 
 from conftest import read_tables
 from inputs import graphs as G
@@ -123,33 +124,79 @@ def test_table5_watts_strogatz_pegp_band():
 
 @pytest.mark.parametrize("kind", ["msp", "pegp"])
 def test_refined_reference(kind):
-    """The parity reference R_X r with iterative refinement (R14):
-    the same operator as the plain apply (dense pseudo-inverse on a tiny
-    well-conditioned case to 1e-13), and on a high-contrast grid it solves
-    L_X z~ = P^T r - mean to an extended-precision residual far below what
-    the unrefined fp64 solve reaches."""
+    """The parity reference R_X r (R14): the same operator as the
+    plain apply (dense pseudo-inverse on a tiny well-conditioned case, 1e-13),
+    and on a high-contrast grid a function of the fp64 edge weights that is
+    well conditioned -- a 1-ulp change of every weight moves it by < 1e-14 --
+    whereas the plain fp64 apply (rounded diagonal, LU) is off by far more."""
     g, h, s = small(6, 0.8, (6, 5), "uniform1_10")
     P = s.P()
+    WX = s.WT if kind == "msp" else s.WH
     LX = s.LT if kind == "msp" else s.LH
     r = G.rhs(g.n, 2)
-    ref = PR.RefinedPreconditioner(P, LX)(r)
-    Rd = PR.dense_R(P, LX)
-    np.testing.assert_allclose(ref, Rd @ r, rtol=0, atol=1e-13 * np.abs(ref).max())
-    g = G.grid2d(40, 30, "loguniform", 8)
-    h = A.build_hierarchy(g, 1)
+    ref = PR.RefinedPreconditioner(P, WX)(r)
+    np.testing.assert_allclose(ref, PR.dense_R(P, LX) @ r, rtol=0, atol=1e-13 * np.abs(ref).max())
+    g = G.grid2d(90, 70, "loguniform", 8)
+    h = A.build_hierarchy(g, 11)
     s = E.expand_msp_only(g, h, 0.8) if kind == "msp" else E.expand(g, h, 0.8)
-    LX = s.LT if kind == "msp" else s.LH
-    Rf = PR.RefinedPreconditioner(s.P(), LX)
+    WX = sp.csr_matrix(s.WT if kind == "msp" else s.WH)
     r = G.rhs(g.n, 3)
-    rt = PR._ld_matvec(Rf.PT, r)
-    rt = rt - rt.mean()
-    z0 = PR.PinvSolver(LX)(np.asarray(rt, dtype=np.float64))
-    zf = Rf.inv(np.asarray(rt, dtype=np.float64)).astype(np.longdouble)
-    for _ in range(6):
-        zf = zf + Rf.inv(np.asarray(rt - PR._ld_matvec(LX, zf), dtype=np.float64))
-    res0 = np.abs(np.asarray(rt - PR._ld_matvec(LX, z0), dtype=np.float64)).max()
-    resf = np.abs(np.asarray(rt - PR._ld_matvec(LX, zf), dtype=np.float64)).max()
-    assert resf < 1e-2 * res0, (resf, res0)
-    out = Rf(r)
+    Rf = PR.RefinedPreconditioner(s.P(), WX)
+    z0 = Rf(r)
     assert Rf.steps >= 1
-    np.testing.assert_allclose(out, PR.Preconditioner(s.P(), LX)(r), rtol=0, atol=1e-9 * np.abs(out).max())
+    Wp = sp.triu(WX, 1).tocoo()
+    Wp.data = Wp.data * (1 + 1.1e-16 * np.random.default_rng(0).choice([-1, 1], Wp.data.size))
+    z1 = PR.RefinedPreconditioner(s.P(), (Wp + Wp.T).tocsr())(r)
+    rel = lambda a, b: float(np.abs(a - b).max() / np.abs(b).max())
+    assert rel(z1, z0) < 1e-14
+    zp = PR.Preconditioner(s.P(), s.LT if kind == "msp" else s.LH)(r)
+    assert 1e-14 < rel(zp, z0) < 1e-9
+
+
+def _exact_R(P, W, r):
+    """R r = P L^+ P^T r in exact rational arithmetic from the fp64 data
+    (fractions.Fraction; tiny graphs only): L = D - W with the exact
+    diagonal, grounded at node 0, minimum-norm shift."""
+    from fractions import Fraction as F
+    Pd = P.toarray()
+    Wd = W.toarray()
+    nt = Wd.shape[0]
+    rt = [sum(F(Pd[i, j]) * F(r[i]) for i in range(Pd.shape[0])) for j in range(nt)]
+    m = sum(rt) / nt
+    rt = [v - m for v in rt]
+    L = [[-F(Wd[i, j]) if i != j else F(0) for j in range(nt)] for i in range(nt)]
+    for i in range(nt):
+        L[i][i] = -sum(L[i][j] for j in range(nt) if j != i)
+    A_ = [row[1:] + [rt[i]] for i, row in enumerate(L)][1:]     # grounded system
+    k = nt - 1
+    for c in range(k):
+        piv = next(i for i in range(c, k) if A_[i][c] != 0)
+        A_[c], A_[piv] = A_[piv], A_[c]
+        for i in range(c + 1, k):
+            f = A_[i][c] / A_[c][c]
+            if f:
+                A_[i] = [a - f * b for a, b in zip(A_[i], A_[c])]
+    z = [F(0)] * k
+    for i in range(k - 1, -1, -1):
+        z[i] = (A_[i][k] - sum(A_[i][j] * z[j] for j in range(i + 1, k))) / A_[i][i]
+    z = [F(0)] + z
+    mz = sum(z) / nt
+    z = [v - mz for v in z]
+    return np.array([float(sum(F(Pd[i, j]) * z[j] for j in range(nt))) for i in range(Pd.shape[0])])
+
+
+@pytest.mark.parametrize("mu", [0.8, None])
+def test_refined_reference_against_exact_rationals(mu):
+    """The refined reference equals R r computed in exact rational
+    arithmetic from the same fp64 weights -- including mu = 1/sqrt(n), where
+    the weights span mu^(2(l-1)) and the plain fp64 apply is meaningless."""
+    g = G.grid2d(4, 3, "loguniform", 5)
+    mu = 1 / np.sqrt(g.n) if mu is None else mu
+    h = A.build_hierarchy(g, 3)
+    s = E.expand_msp_only(g, h, mu)
+    r = G.rhs(g.n, 4)
+    Rf = PR.msp_refined(s)
+    z = Rf(r)
+    ze = _exact_R(s.P(), sp.csr_matrix(s.WT), r)
+    assert h.nlevels >= 3 and Rf.steps < Rf.max_steps
+    np.testing.assert_allclose(z, ze, rtol=0, atol=4e-16 * np.abs(ze).max())
