@@ -179,27 +179,65 @@ def rgg(npts: int, mean_degree: float = 12.0, seed: int = 0) -> Graph:
     return largest_component(npts, u, v, w, name=f"rgg_{npts}")
 
 
-def chung_lu(n: int, exponent: float = 2.1, mean_degree: float = 16.0, seed: int = 0,
-             weights: str = "uniform0.5_2") -> Graph:
-    """Chung-Lu power-law graph (configs[4]): expected degrees
-    d_i proportional to (i+1)^(-1/(exponent-1)) scaled to the requested mean,
-    m = n*mean/2 endpoint pairs drawn i.i.d. with probability d_i/sum(d);
-    self loops and duplicate pairs dropped; weights uniform[0.5,2];
-    largest connected component only."""
-    rng = np.random.default_rng(seed)
+# ---- counter-based uniforms (splitmix64), shared by the host generator below
+# and the device generator in inputs/device.py so both draw the same graph
+SM_GAMMA = 0x9E3779B97F4A7C15
+SM_M1 = 0xBF58476D1CE4E5B9
+SM_M2 = 0x94D049BB133111EB
+
+
+def splitmix64_np(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser of x + gamma (uint64 in, uint64 out, wraps mod 2^64)."""
+    z = np.asarray(x, dtype=np.uint64) + np.uint64(SM_GAMMA)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(SM_M1)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(SM_M2)
+    return z ^ (z >> np.uint64(31))
+
+
+def stream_key(seed: int, stream: int) -> int:
+    """64-bit key of one random stream of one seed."""
+    return int(splitmix64_np(np.array([(seed * 0x100000001B3 + stream) & (2**64 - 1)], dtype=np.uint64))[0])
+
+
+def uniform01_np(key: int, idx: np.ndarray) -> np.ndarray:
+    """U[0,1) number idx of the stream `key`: top 53 bits of splitmix64(key ^ idx)."""
+    z = splitmix64_np(np.uint64(key) ^ np.asarray(idx, dtype=np.uint64))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def chung_lu_cdf(n: int, exponent: float = 2.1, mean_degree: float = 16.0) -> np.ndarray:
+    """Normalised cumulative expected degrees d_i ~ (i+1)^(-1/(exponent-1))
+    (the host computes it for both generators)."""
     d = (np.arange(1, n + 1, dtype=np.float64)) ** (-1.0 / (exponent - 1.0))
     d *= mean_degree * n / d.sum()
     cdf = np.cumsum(d)
     cdf /= cdf[-1]
+    return cdf
+
+
+def chung_lu(n: int, exponent: float = 2.1, mean_degree: float = 16.0, seed: int = 0,
+             weights: str = "uniform0.5_2") -> Graph:
+    """Chung-Lu power-law graph (configs[4]): expected degrees
+    d_i proportional to (i+1)^(-1/(exponent-1)) scaled to the requested mean;
+    m = n*mean/2 endpoint pairs, endpoint j of pair e drawn by inverting the
+    degree cdf at U(stream 1, 2e + j); self loops and duplicate pairs
+    dropped; weight of the k-th distinct edge (sorted by (min, max))
+    0.5 + 1.5 U(stream 2, k); largest connected component only.  Counter-
+    based uniforms, so inputs/device.py draws the identical graph on a GPU."""
+    cdf = chung_lu_cdf(n, exponent, mean_degree)
     m = int(n * mean_degree / 2)
-    a = np.searchsorted(cdf, rng.random(m), side="right").astype(np.int64)
-    b = np.searchsorted(cdf, rng.random(m), side="right").astype(np.int64)
+    k1 = stream_key(seed, 1)
+    e = np.arange(m, dtype=np.uint64)
+    a = np.searchsorted(cdf, uniform01_np(k1, 2 * e), side="right").astype(np.int64)
+    b = np.searchsorted(cdf, uniform01_np(k1, 2 * e + np.uint64(1)), side="right").astype(np.int64)
     a = np.minimum(a, n - 1); b = np.minimum(b, n - 1)
     keep = a != b
     lo = np.minimum(a[keep], b[keep]); hi = np.maximum(a[keep], b[keep])
     key = np.unique(lo * n + hi)
     lo, hi = key // n, key % n
-    w = _weights(weights, lo.size, rng)
+    if weights != "uniform0.5_2":
+        raise ValueError(weights)
+    w = 0.5 + 1.5 * uniform01_np(stream_key(seed, 2), np.arange(key.size, dtype=np.uint64))
     return largest_component(n, lo, hi, w, name=f"chunglu_{n}")
 
 

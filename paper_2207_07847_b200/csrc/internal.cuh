@@ -134,6 +134,13 @@ struct Handle {
   DBuf<double> sell_w;
   DBuf<uint32_t> sell_mask;
   DBuf<int32_t> long_rows;
+  // huge rows cut into segments (sched.cuh HugeDesc)
+  DBuf<int4> hseg;
+  DBuf<int32_t> hfirst;
+  DBuf<unsigned> hcnt;
+  DBuf<double> hpart;
+  int64_t nhseg = 0;
+  HugeDesc huge_desc() const { return HugeDesc{hseg.p, nhseg, hfirst.p, hcnt.p, hpart.p}; }
 
   // ---- solve schedule: tiers of tile
   // kernels over levels 1..Kc, then one single-CTA kernel for Kc..L

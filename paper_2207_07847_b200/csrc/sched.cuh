@@ -15,6 +15,19 @@
 namespace msp {
 
 constexpr int MAXL = 40;   // levels
+
+// Rows of degree > hcap ("huge", power-law hubs: up to millions of entries)
+// are cut into segments of at most HUGE_SEG entries, a CTA each in the SpMV;
+// the CTA that finishes a row's last segment (ticket cnt[row]) sums the
+// row's partials in segment order (deterministic) and writes the row.
+constexpr int HUGE_SEG = 16384;
+struct HugeDesc {
+  const int4* seg;       // [nseg]: x = huge-row index (into long_rows[nlong + x]), y = e0, z = e1
+  int64_t nseg;
+  const int32_t* first;  // [nhuge + 1]: first segment of each huge row
+  unsigned* cnt;         // [nhuge]: arrival tickets (zero between launches)
+  double* part;          // [nseg]: segment partial sums
+};
 constexpr int MAXT = 16;   // levels per tier
 
 struct Lv {

@@ -427,6 +427,13 @@ __global__ void k_hvec(int64_t nB, const int32_t* __restrict__ cptr, const doubl
   for (int32_t c = cptr[B]; c < cptr[B + 1]; ++c) Gk[c] = ckk * gk[c] + gp;
 }
 
+// (rowptr[r], rowptr[r + 1]) of rows[0..m)
+__global__ void k_row_bounds(int64_t m, const int32_t* __restrict__ rows, const int32_t* __restrict__ rowptr,
+                             int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) { out[2 * i] = rowptr[rows[i]]; out[2 * i + 1] = rowptr[rows[i] + 1]; }
+}
+
 // ------------------------------------------------------------ SELL-32
 __global__ void k_fill_uniform_ptr(int64_t ns, int64_t stride, int64_t* __restrict__ sptr) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1035,6 +1042,45 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 2, fl.p);  // huge rows follow the long ones
     MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p + h.nlong, nsel.p, n, st));
     h.nhuge = d2h_scalar(nsel.p, st);
+    // huge rows cut into segments of <= HUGE_SEG entries (sched.cuh)
+    {
+      std::vector<int32_t> hr(std::max<int64_t>(h.nhuge, 1)), hp(std::max<int64_t>(2 * h.nhuge, 1));
+      if (h.nhuge > 0)
+        MSP_CUDA(cudaMemcpyAsync(hr.data(), h.long_rows.p + h.nlong, h.nhuge * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+      if (h.nhuge > 0) {
+        DBuf<int32_t> bnd;
+        bnd.alloc(2 * h.nhuge);
+        k_row_bounds<<<grid_for(h.nhuge), TPB, 0, st>>>(h.nhuge, h.long_rows.p + h.nlong, h.rowptr1.p, bnd.p);
+        MSP_LAUNCH_CHECK();
+        MSP_CUDA(cudaMemcpyAsync(hp.data(), bnd.p, 2 * h.nhuge * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        MSP_CUDA(cudaStreamSynchronize(st));
+      }
+      std::vector<int4> segs;
+      std::vector<int32_t> first(h.nhuge + 1, 0);
+      for (int64_t i = 0; i < h.nhuge; ++i) {
+        first[i] = (int32_t)segs.size();
+        for (int64_t e = hp[2 * i]; e < hp[2 * i + 1]; e += HUGE_SEG)
+          segs.push_back(make_int4((int)i, (int)e, (int)std::min<int64_t>(e + HUGE_SEG, hp[2 * i + 1]), 0));
+      }
+      first[h.nhuge] = (int32_t)segs.size();
+      h.nhseg = (int64_t)segs.size();
+      if (std::getenv("MSP_VERBOSE"))
+        fprintf(stderr, "[msp] SELL: n=%lld slices=%lld maxw=%d uniform=%d entries=%lld (adjacency %lld) lcap=%d "
+                "long=%lld huge=%lld huge segments=%lld\n", (long long)n, (long long)ns, h.sell_maxw,
+                (int)h.sell_uniform, (long long)tot, (long long)h.nnz_adj, lcap, (long long)h.nlong,
+                (long long)h.nhuge, (long long)h.nhseg);
+      h.hseg.alloc(std::max<size_t>(segs.size(), 1));
+      h.hfirst.alloc(h.nhuge + 1);
+      h.hcnt.alloc(std::max<int64_t>(h.nhuge, 1));
+      h.hpart.alloc(std::max<size_t>(segs.size(), 1));
+      if (!segs.empty())
+        MSP_CUDA(cudaMemcpyAsync(h.hseg.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+      MSP_CUDA(cudaMemcpyAsync(h.hfirst.p, first.data(), first.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      MSP_CUDA(cudaMemsetAsync(h.hcnt.p, 0, std::max<int64_t>(h.nhuge, 1) * sizeof(unsigned), st));
+      MSP_CUDA(cudaStreamSynchronize(st));
+    }
   }
 
   clk.mark(st, "SELL");

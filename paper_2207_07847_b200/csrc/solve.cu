@@ -352,6 +352,23 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col, const
   return (a0 + a1) + (a2 + a3);
 }
 
+// Huge-row segment s of huge row hr done with block sum acc (thread 0): true
+// in the CTA that completes the row, with the row total (partials summed in
+// segment order, so the result does not depend on arrival order)
+__device__ __forceinline__ bool huge_last(const HugeDesc& hd, int hr, int64_t s, double acc, double* tot) {
+  hd.part[s] = acc;
+  __threadfence();
+  const int f0 = hd.first[hr], f1 = hd.first[hr + 1];
+  const unsigned t = atomicAdd(&hd.cnt[hr], 1u);
+  if (t != (unsigned)(f1 - f0 - 1)) return false;
+  __threadfence();
+  double a = 0.0;
+  for (int k = f0; k < f1; ++k) a += __ldcg(hd.part + k);
+  hd.cnt[hr] = 0;
+  *tot = a;
+  return true;
+}
+
 // PCG scalars after the level-1 output: rz = (r, R r)
 __device__ __forceinline__ void finish_rz(double rz, double* scal, int mode) {
   if (mode == M_ITER) scal[S_BETA] = rz / scal[S_RHO];
@@ -394,7 +411,7 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ perm, const dou
 template <bool PCG>
 __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                               const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                              const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
+                                              const uint32_t* __restrict__ smask, int64_t nlong, const HugeDesc hd,
                                               const int32_t* __restrict__ long_rows,
                                               const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                               const double* __restrict__ w, const double* __restrict__ z,
@@ -456,20 +473,22 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
       }
     }
   }
-  for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
-    const int64_t r = long_rows[nlong + i];
+  for (int64_t s = blockIdx.x; s < hd.nseg; s += gridDim.x) {  // CTA per huge-row segment
+    const int4 sg = hd.seg[s];
+    const int64_t r = long_rows[nlong + sg.x];
     if (r < row0 || r >= row1) continue;  // block-uniform
     const double po = PCG ? pold[r] : 0.0;
     const double pi = PCG ? z[r] + beta * po : z[r];
-    double acc = row_dot<TPB>(col, w, rowptr[r], rowptr[r + 1], threadIdx.x, pi,
+    double acc = row_dot<TPB>(col, w, sg.y, sg.z, threadIdx.x, pi,
                               [&](int32_t j) { return PCG ? z[j] + beta * pold[j] : z[j]; });
     acc = block_sum<TPB>(acc);
-    if (threadIdx.x == 0) {
-      q[r] = acc;
+    double tot;
+    if (threadIdx.x == 0 && huge_last(hd, sg.x, s, acc, &tot)) {
+      q[r] = tot;
       if (PCG) {
         pnew[r] = pi;
         x[r] += alpha * po;
-        d += pi * acc;
+        d += pi * tot;
       }
     }
   }
@@ -498,7 +517,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 template <int MW, bool UNIF>
 __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
-                                                      const uint32_t* __restrict__ smask, int64_t nlong, int64_t nhuge,
+                                                      const uint32_t* __restrict__ smask, int64_t nlong, const HugeDesc hd,
                                                       const int32_t* __restrict__ long_rows,
                                                       const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                       const double* __restrict__ w, const double2* __restrict__ zp,
@@ -620,21 +639,23 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
       d += pi * acc;
     }
   }
-  for (int64_t i = blockIdx.x; i < nhuge; i += gridDim.x) {  // CTA per huge row
-    const int64_t row = long_rows[nlong + i];
+  for (int64_t s = blockIdx.x; s < hd.nseg; s += gridDim.x) {  // CTA per huge-row segment
+    const int4 sg = hd.seg[s];
+    const int64_t row = long_rows[nlong + sg.x];
     const double2 vr = zp[row];
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
-    double acc = row_dot<TPB>(col, w, rowptr[row], rowptr[row + 1], threadIdx.x, pi, [&](int32_t j) {
+    double acc = row_dot<TPB>(col, w, sg.y, sg.z, threadIdx.x, pi, [&](int32_t j) {
       const double2 v = zp[j];
       return v.x + beta * v.y;
     });
     acc = block_sum<TPB>(acc);
-    if (threadIdx.x == 0) {
-      q[row] = acc;
+    double tot;
+    if (threadIdx.x == 0 && huge_last(hd, sg.x, s, acc, &tot)) {
+      q[row] = tot;
       zpout[2 * row + 1] = pi;
       x[row] += alpha * pr;
-      d += pi * acc;
+      d += pi * tot;
     }
   }
   TRACE(2);
@@ -2219,7 +2240,7 @@ template <bool PCG>
 void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
                  cudaStream_t st) {
   launch_c(1, k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-         (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
+         (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
          (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
          (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, (int64_t)0, h.n);
   ++h.launches;
@@ -2229,7 +2250,7 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
 void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
   auto go = [&](auto kern) {
     launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
-           (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge, (const int32_t*)h.long_rows.p,
+           (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(), (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
   };
@@ -2707,7 +2728,7 @@ void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x
                "alltoallv(p halo)");
     if (nrecv) k_put<<<grid_for(nrecv), TPB, 0, st>>>(nrecv, d.recv_idx.p, d.recvbuf.p, h.vp.p);
     launch(k_spmv<false>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.nhuge,
+           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
            (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
            (const double*)h.w1.p, (const double*)h.vp.p, (const double*)nullptr, (double*)nullptr, h.vq.p,
            (double*)nullptr, h.red.p, h.scal.p, h.counters.p, d.row0, d.row1);

@@ -42,3 +42,17 @@ def test_rhs_orthogonal_to_ones():
     b = G.rhs(1000, 3)
     assert abs(b.sum()) < 1e-10
     assert G.rhs_paper(8).sum() == 0 and G.rhs_paper(8)[-1] == -7
+
+
+def test_chung_lu_device_recipe_matches_host_on_cpu():
+    """inputs.device draws configs[4]'s Chung-Lu graph with torch (on the GPU
+    at full size); run here on the CPU it yields the host generator's CSR
+    bit for bit (counter-based uniforms, same dedup / weights / LCC)."""
+    import torch
+    from inputs import device as D
+    g = G.chung_lu(20000, 2.1, 16.0, 5)
+    n, rp, c, v = D.chung_lu_csr(20000, 2.1, 16.0, 5, "cpu")
+    assert n == g.n
+    assert np.array_equal(rp.numpy(), g.rowptr) and np.array_equal(c.numpy(), g.col)
+    assert np.array_equal(v.numpy(), g.val)
+    assert c.dtype == torch.int32 and v.dtype == torch.float64

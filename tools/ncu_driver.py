@@ -22,12 +22,13 @@ def main():
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--precond", default="msp")
     ap.add_argument("--mu", type=float, default=0.8)
+    ap.add_argument("--scale", type=float, default=1.0)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    g = G.config_graph(a.config)
-    S = M.setup(g.n, torch.as_tensor(g.rowptr, device=dev), torch.as_tensor(g.col, device=dev),
-                torch.as_tensor(g.val, device=dev), mu=a.mu)
-    b = torch.as_tensor(G.rhs(g.n, 0), device=dev)
+    from inputs import device as D
+    n, rp, col, val = D.config_csr(a.config, a.scale, 0, dev)
+    S = M.setup(n, rp, col, val, mu=a.mu)
+    b = torch.as_tensor(G.rhs(n, 0), device=dev)
     x = torch.empty_like(b)
     rep = S.pcg_solve(b, x, rtol=1e-8, maxit=a.iters, precond=a.precond)
     torch.cuda.synchronize()
