@@ -195,48 +195,55 @@ int msp_set_profiling(msp_handle* h, int on);
 int msp_get_profile(msp_handle* h, double* ms, int64_t* counts);
 
 /*
- * Multi-GPU solve (row 6 of DESIGN.md §8; "Multi-GPU").  One process per GPU;
- * every rank calls msp_setup on the full graph (same seed: identical
- * hierarchy, bit for bit), then the ranks solve ONE system together: rank r
- * owns a contiguous range of the first tier's tiles (level-1 rows and their
- * subtrees up to that tier's top level); the levels above are replicated.
- * Exchanges per PCG iteration: the SpMV halo (p of the neighbour rows), the
- * all-gather of y at the first tier's top level, and all-reduces of (p, q),
- * ((r, r), gdot) and (r, z).  The library does not link a communication
- * library: the caller supplies the collectives as callbacks on device
- * buffers (e.g. torch.distributed over NCCL), invoked on `stream`'s order.
+ * Multi-GPU solve (row 6 of DESIGN.md §8).  One process
+ * per GPU; every rank calls msp_setup on the full graph (same seed: the same
+ * hierarchy, bit for bit), then msp_dist_init, then the ranks solve ONE
+ * system together.  Partition: the nodes of a partition level kp (the top of
+ * the highest solve tier with >= 32 nodes per rank) are split into
+ * contiguous ranges balanced by the rows' work (adjacency entries + 8 per
+ * row); by the nested numbering rank r then owns a contiguous range of every
+ * level k <= kp, down to its level-1 rows; levels above kp are replicated.
+ * Per PCG iteration (all stream-ordered, no host synchronisation): halo
+ * exchange of p (NCCL send/recv), all-reduce of (p, q), all-gather of
+ * [y_kp own range, (r, r), gdot], all-reduce of (r, R r).  Iterations run in
+ * captured CUDA graphs; the host reads the done flag once per 64.
  *
- * msp_partition_plan -- host-only (no GPU calls): the partition and halo plan
- *   of `rank`.  rowptr/col: the level-1 nested CSR (n+1 / nnz entries, host),
- *   tile_rows: the first row of every first-tier tile (ntiles+1 entries).
- *   Out: range[4] = (row0, row1, tile0, tile1); recv_counts[world] halo rows
- *   received from each peer, send_counts[world] rows sent to each peer;
- *   recv_rows (sorted, grouped by owner) and send_rows (grouped by peer,
- *   sorted) if non-NULL with the given capacities.
- * msp_dist_solve -- PCG-MSP (reading R10) on the partitioned system.  b, x:
- *   the FULL vectors in the original numbering (host or device per `mem`);
- *   each rank reads b's own rows; x receives the solution on the rank's own
- *   rows and 0 elsewhere (a sum over ranks assembles it).
- *   report as msp_pcg_solve (iterations identical on all ranks).
- *   Errors: MSP_ERR_UNSUPPORTED if the hierarchy has no tiled first tier.
+ * msp_dist_unique_id -- fills id128 (128 bytes, an NCCL unique id); rank 0
+ *   calls it and the caller broadcasts the bytes (e.g. torch.distributed).
+ * msp_dist_init -- the partition, halo plan and NCCL communicator of `rank`
+ *   (1 <= world <= 16); collective over the ranks (NCCL init).  Errors:
+ *   MSP_ERR_UNSUPPORTED when the graph is too small for `world` ranks.
+ * msp_dist_range -- out[8] = (row0, row1, kp, tp, nsend, nrecv, world, rank)
+ *   of the handle's rank; rows in the nested numbering.
+ * msp_dist_solve -- PCG-MSP (reading R10) on the partitioned system.  b: the
+ *   FULL rhs in the original numbering (host or device per `mem`, the same
+ *   on every rank); x receives the solution on the rank's own rows and 0
+ *   elsewhere (a sum over ranks assembles it).  report as msp_pcg_solve
+ *   (identical on every rank).  MSP_ERR_UNSUPPORTED for graphs whose SELL
+ *   slices are wider than 16 (the pair SpMV).
+ * msp_dist_group_solve -- the same decomposition for `world` ranks driven by
+ *   ONE process on one device (handles hs[0..world), each set up on the same
+ *   graph): the collectives become device copies and fixed-order sums on one
+ *   stream, nothing waits on anything.  For tests of the partitioned
+ *   arithmetic on a single GPU; x is the assembled solution.
+ * msp_dist_boundaries / msp_halo_plan -- host-only (no GPU calls) parts of
+ *   the plan: quantile boundaries of a non-decreasing prefix cost[m+1] into
+ *   bnd[world+1] (MSP_ERR_UNSUPPORTED if a rank would own nothing); the halo
+ *   of `rank` given level-1 row boundaries row_bnd[world+1] and the nested
+ *   CSR (host): rows received from / sent to each peer (counts, and the
+ *   sorted rows if the buffers are non-NULL).
  */
-typedef int (*msp_allreduce_fn)(double* dev, int64_t n, void* ctx);           /* in-place sum */
-typedef int (*msp_allgather_fn)(const double* dev_send, double* dev_recv, int64_t n_each, void* ctx);
-typedef int (*msp_alltoallv_fn)(const double* dev_send, const int64_t* send_counts, double* dev_recv,
-                                const int64_t* recv_counts, void* ctx);
-typedef struct msp_comm {
-  int32_t world, rank;
-  msp_allreduce_fn allreduce;
-  msp_allgather_fn allgather;   /* rank-ordered, n_each per rank, dev_recv = world * n_each */
-  msp_alltoallv_fn alltoallv;   /* counts in elements, rank-ordered */
-  void* ctx;
-} msp_comm;
-int msp_partition_plan(int64_t n, const int32_t* rowptr, const int32_t* col, int64_t ntiles,
-                       const int32_t* tile_rows, int32_t world, int32_t rank, int64_t* range,
-                       int64_t* recv_counts, int64_t* send_counts, int64_t* recv_rows, int64_t recv_cap,
-                       int64_t* send_rows, int64_t send_cap);
-int msp_dist_solve(msp_handle* h, const msp_comm* comm, const double* b, double* x, double rtol, int32_t maxit,
-                   int mem, void* stream, msp_report* report);
+int msp_dist_unique_id(void* id128);
+int msp_dist_init(msp_handle* h, int32_t world, int32_t rank, const void* id128, void* stream);
+int msp_dist_range(msp_handle* h, int64_t* out8);
+int msp_dist_solve(msp_handle* h, const double* b, double* x, double rtol, int32_t maxit, int mem, void* stream,
+                   msp_report* report);
+int msp_dist_group_solve(msp_handle** hs, int32_t world, const double* b, double* x, double rtol, int32_t maxit,
+                         int mem, void* stream, msp_report* report);
+int msp_dist_boundaries(int64_t m, const int64_t* cost, int32_t world, int64_t* bnd);
+int msp_halo_plan(int64_t n, const int32_t* rowptr, const int32_t* col, int32_t world, const int64_t* row_bnd,
+                  int32_t rank, int64_t* recv_counts, int64_t* send_counts, int64_t* recv_rows, int64_t recv_cap,
+                  int64_t* send_rows, int64_t send_cap);
 
 /* Thread-local description of the last error (never NULL). */
 const char* msp_last_error(void);

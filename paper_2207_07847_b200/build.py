@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, extra=None, lib=None) -> s
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [NVCC, "-shared", *ARCH, "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    cmd = [NVCC, "-shared", *ARCH, "-o", lib, *objs, "-lnccl", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     subprocess.check_call(cmd)
     return lib
 

@@ -1,6 +1,7 @@
 // capi.cu -- extern "C" boundary of libmsp_b200.so (declared in
 // include/msp_b200.h).  Argument checking and host<->device marshalling only;
 // every step of the method runs in the kernels of setup.cu / solve.cu.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <vector>
@@ -338,30 +339,105 @@ int msp_solve_LH(msp_handle* H, const double* r, double* z, int mem, void* strea
   });
 }
 
-int msp_dist_solve(msp_handle* H, const msp_comm* comm, const double* b, double* x, double rtol, int32_t maxit,
-                   int mem, void* stream, msp_report* rep) {
+int msp_dist_unique_id(void* id128) {
   return guarded([&] {
-    need(H && comm && b && x, "null argument");
-    need(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world, "bad rank / world");
-    need(comm->allreduce && comm->allgather && comm->alltoallv, "missing communication callback");
+    need(id128 != nullptr, "null argument");
+    msp::dist_unique_id(id128);
+  });
+}
+
+int msp_dist_init(msp_handle* H, int32_t world, int32_t rank, const void* id128, void* stream) {
+  return guarded([&] {
+    need(H != nullptr, "null handle");
+    need(world >= 1 && world <= 16 && rank >= 0 && rank < world, "bad world / rank");
+    Handle& h = H->h;
+    if (h.dist) { msp::dist_free(h.dist); h.dist = nullptr; }
+    h.dist = msp::dist_build(h, world, rank, id128, S(stream));
+  });
+}
+
+int msp_dist_range(msp_handle* H, int64_t* out) {
+  return guarded([&] {
+    need(H && out, "null argument");
+    need(H->h.dist != nullptr, "msp_dist_init was not called");
+    msp::dist_range(H->h, out);
+  });
+}
+
+namespace {
+// b (caller numbering, host or device) into every handle's vb; x out as the
+// sum of the handles' own rows
+void dist_io_in(std::vector<Handle*>& hs, const double* b, int mem, cudaStream_t st) {
+  for (Handle* hp : hs) {
+    const double* bd = stage_in(*hp, b, mem, hp->stage_in, st);
+    msp::gather_to_nested(*hp, bd, hp->vb.p, st);
+  }
+}
+}  // namespace
+
+int msp_dist_solve(msp_handle* H, const double* b, double* x, double rtol, int32_t maxit, int mem, void* stream,
+                   msp_report* rep) {
+  return guarded([&] {
+    need(H && b && x, "null argument");
     need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
     need(rtol >= 0 && maxit >= 0, "bad rtol / maxit");
     Handle& h = H->h;
+    need(h.dist != nullptr, "msp_dist_init was not called");
     cudaStream_t st = S(stream);
-    const double* bd = stage_in(h, b, mem, h.stage_in, st);
-    msp::gather_to_nested(h, bd, h.vb.p, st);
-    msp::pcg_dist_nested(h, *comm, h.vb.p, h.vx.p, rtol, maxit, st, rep);
-    // keep own rows only (the rest of vx is stale): zero elsewhere
-    msp::zero_outside(h, h.vx.p, st);
+    std::vector<Handle*> hs{&h};
+    dist_io_in(hs, b, mem, st);
+    msp::pcg_dist_group(hs, false, rtol, maxit, st, rep);
     if (mem == MSP_MEM_DEVICE) {
       msp::scatter_from_nested(h, h.vx.p, x, st);
-      MSP_CUDA(cudaStreamSynchronize(st));
     } else {
       if (h.stage_out.n < (size_t)h.n) h.stage_out.alloc(h.n);
       msp::scatter_from_nested(h, h.vx.p, h.stage_out.p, st);
       MSP_CUDA(cudaMemcpyAsync(x, h.stage_out.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, st));
-      MSP_CUDA(cudaStreamSynchronize(st));
     }
+    MSP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int msp_dist_group_solve(msp_handle** Hs, int32_t world, const double* b, double* x, double rtol, int32_t maxit,
+                         int mem, void* stream, msp_report* rep) {
+  return guarded([&] {
+    need(Hs && b && x, "null argument");
+    need(world >= 1 && world <= 16, "world must be 1..16");
+    need(mem == MSP_MEM_DEVICE || mem == MSP_MEM_HOST, "bad mem");
+    need(rtol >= 0 && maxit >= 0, "bad rtol / maxit");
+    cudaStream_t st = S(stream);
+    std::vector<Handle*> hs;
+    for (int r = 0; r < world; ++r) {
+      need(Hs[r] != nullptr, "null handle");
+      Handle& h = Hs[r]->h;
+      need(h.n == Hs[0]->h.n && h.n_tilde == Hs[0]->h.n_tilde, "handles of different graphs");
+      if (h.dist) { msp::dist_free(h.dist); h.dist = nullptr; }
+      h.dist = msp::dist_build(h, world, r, nullptr, st);
+      hs.push_back(&h);
+    }
+    dist_io_in(hs, b, mem, st);
+    msp::pcg_dist_group(hs, true, rtol, maxit, st, rep);
+    // assemble: the sum of the ranks' own rows (each zero outside its rows)
+    Handle& h0 = *hs[0];
+    for (int r = 1; r < world; ++r) msp::add_into(h0, hs[r]->vx.p, h0.vx.p, st);
+    if (mem == MSP_MEM_DEVICE) {
+      msp::scatter_from_nested(h0, h0.vx.p, x, st);
+    } else {
+      if (h0.stage_out.n < (size_t)h0.n) h0.stage_out.alloc(h0.n);
+      msp::scatter_from_nested(h0, h0.vx.p, h0.stage_out.p, st);
+      MSP_CUDA(cudaMemcpyAsync(x, h0.stage_out.p, h0.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    MSP_CUDA(cudaStreamSynchronize(st));
+    for (Handle* hp : hs) { msp::dist_free(hp->dist); hp->dist = nullptr; }
+  });
+}
+
+// debugging aid (not in the header): the device scalars of the last solve
+int msp_debug_scalars(msp_handle* H, double* out, int64_t n) {
+  return guarded([&] {
+    need(H && out && n > 0, "null argument");
+    MSP_CUDA(cudaMemcpy(out, H->h.scal.p, std::min<int64_t>(n, (int64_t)H->h.scal.n) * sizeof(double),
+                        cudaMemcpyDeviceToHost));
   });
 }
 

@@ -77,6 +77,9 @@ struct LevelHost {
   int64_t off = 0;        // offset of level k in the expanded (n~) vector
 };
 
+struct DistRank;                 // dist_solve.cuh: one rank's partition, plan and communicator
+void dist_free(DistRank* d);
+
 // Device-resident state of a handle.
 struct Handle {
   // ---- problem
@@ -180,7 +183,7 @@ struct Handle {
   double pegp_rtol = 1e-13;
   int pegp_maxit = 5000;
   int pegp_last_inner = 0;
-  int64_t dist_row0 = 0, dist_row1 = 0;  // own rows of the last msp_dist_solve
+  DistRank* dist = nullptr;   // msp_dist_init / the loopback group
 
   // ---- solve workspaces
   DBuf<double> Y, Z, W;       // n~-layout sweep vectors (y = P^T sums, z, w)
@@ -208,6 +211,7 @@ struct Handle {
   Handle() = default;
   Handle(const Handle&) = delete;
   ~Handle() {
+    if (dist) dist_free(dist);
     if (graph) cudaGraphExecDestroy(graph);
     if (pegp_graph) cudaGraphExecDestroy(pegp_graph);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -228,9 +232,11 @@ void gather_to_nested(Handle& h, const double* src_orig, double* dst_nested, cud
 void scatter_from_nested(Handle& h, const double* src_nested, double* dst_orig, cudaStream_t st);
 void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol, int maxit,
                 cudaStream_t st, msp_report* rep);
-void zero_outside(Handle& h, double* x, cudaStream_t st);
-void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x, double rtol, int maxit,
-                     cudaStream_t st, msp_report* rep);
+DistRank* dist_build(Handle& h, int world, int rank, const void* id128, cudaStream_t st);
+void pcg_dist_group(std::vector<Handle*>& hs, bool loop, double rtol, int maxit, cudaStream_t st, msp_report* rep);
+void dist_unique_id(void* id128);
+void dist_range(const Handle& h, int64_t* out8);
+void add_into(Handle& h, const double* a, double* y, cudaStream_t st);
 void alloc_solve_workspace(Handle& h);
 void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
 // pegp.cu
@@ -246,5 +252,7 @@ void release_graph(Handle& h);
 void build_coarse_matrix(Handle& h, cudaStream_t st);  // solve.cu
 void build_top_map(Handle& h, cudaStream_t st);        // solve.cu
 CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv);  // setup.cu
+std::vector<int4> make_tile_segs(const Handle& h, int k0, int nl, const TierDesc& d, const std::vector<int32_t>& ts,
+                                 int64_t ntiles);                   // setup.cu
 
 }  // namespace msp

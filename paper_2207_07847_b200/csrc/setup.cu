@@ -1205,6 +1205,49 @@ CoarseDesc coarse_desc(const Handle& h, int Kc, bool stage_pinv) {
 }
 
 
+// Static TMA segments (sched.cuh) of tiles whose starts per level are
+// ts[u * (ntiles + 1) + j] (host copy), for the down kernel of tier k0.. with
+// nl levels and layout d: the kernel stages them without computing windows.
+std::vector<int4> make_tile_segs(const Handle& h, int k0_, int nl, const TierDesc& d, const std::vector<int32_t>& ts,
+                                 int64_t ntiles) {
+  const int S = 3 * (nl - 1) + (k0_ > 1 ? 1 : 0);
+  const int64_t nt1 = ntiles + 1;
+  std::vector<int4> segs((size_t)ntiles * S);
+  const int64_t n1 = h.lv[0].n;
+  for (int64_t j = 0; j < ntiles; ++j) {
+    auto sa = [&](int u) { return (int64_t)ts[(size_t)u * nt1 + j]; };
+    auto sn = [&](int u) { return (int64_t)ts[(size_t)u * nt1 + j + 1] - sa(u); };
+    int g = 0;
+    auto put = [&](int kind, int tt, int dst, int es, int64_t lo, int64_t hi) {
+      const int64_t m = (es == 4) ? 3 : 1;
+      const int64_t a0 = lo & ~m;
+      const int64_t e0 = (hi + m) & ~m;
+      const int64_t bytes = (hi > lo) ? (e0 - a0) * es : 0;
+      if (a0 > INT32_MAX || bytes > INT32_MAX) throw Error{MSP_ERR_UNSUPPORTED, "segment offset >= 2^31"};
+      segs[(size_t)j * S + g++] = make_int4(kind | (tt << 2) | (dst << 8), (int)bytes, (int)a0, (int)(lo - a0));
+    };
+    for (int u = 1; u < nl; ++u) {
+      const int64_t base = h.cptr_off[k0_ + u - 2];
+      put(SEG_CP, u, d.o_cp[u], 4, base + sa(u), base + sa(u) + sn(u) + 1);
+    }
+    for (int u = 1; u < nl; ++u) {
+      const int64_t base = 3 * (h.lv[k0_ + u - 1].off - n1 + sa(u));
+      put(SEG_KI, u, d.o_ki[u], 8, base, base + 3 * sn(u));
+    }
+    for (int u = 0; u + 1 < nl; ++u) {
+      const int64_t lo0 = sa(u) - 2 * sa(u + 1);
+      const int64_t lo1 = (sa(u) + sn(u)) - 2 * (sa(u + 1) + sn(u + 1));
+      const int64_t base = 3 * h.lo_off[k0_ + u - 1];
+      put(SEG_LO, u, d.o_lo[u], 8, base + 3 * lo0, base + 3 * lo1);
+    }
+    if (k0_ > 1) {
+      const int64_t base = h.lv[k0_ - 1].off;
+      put(SEG_N0, 0, d.o_n[0], 8, base + sa(0), base + sa(0) + sn(0));
+    }
+  }
+  return segs;
+}
+
 // Tiers and tiles of the solve schedule.
 void build_schedule(Handle& h, cudaStream_t st) {
   const int L = h.levels;
@@ -1304,41 +1347,8 @@ void build_schedule(Handle& h, cudaStream_t st) {
       t.desc.tpc = 1;  // first tier: set in alloc_solve_workspace (needs the occupancy)
       // static TMA segments of every tile of the down kernel (sched.cuh)
       {
-        const int S = 3 * (nl - 1) + (k0_ > 1 ? 1 : 0);
-        t.desc.nseg = S;
-        std::vector<int4> segs((size_t)t.ntiles * S);
-        const int64_t n1 = h.lv[0].n;
-        for (int64_t j = 0; j < t.ntiles; ++j) {
-          auto sa = [&](int u) { return (int64_t)ts[(size_t)u * nt1 + j]; };
-          auto sn = [&](int u) { return (int64_t)ts[(size_t)u * nt1 + j + 1] - sa(u); };
-          int g = 0;
-          auto put = [&](int kind, int tt, int dst, int es, int64_t lo, int64_t hi) {
-            const int64_t m = (es == 4) ? 3 : 1;
-            const int64_t a0 = lo & ~m;
-            const int64_t e0 = (hi + m) & ~m;
-            const int64_t bytes = (hi > lo) ? (e0 - a0) * es : 0;
-            if (a0 > INT32_MAX || bytes > INT32_MAX) throw Error{MSP_ERR_UNSUPPORTED, "segment offset >= 2^31"};
-            segs[(size_t)j * S + g++] = make_int4(kind | (tt << 2) | (dst << 8), (int)bytes, (int)a0, (int)(lo - a0));
-          };
-          for (int u = 1; u < nl; ++u) {
-            const int64_t base = h.cptr_off[k0_ + u - 2];
-            put(SEG_CP, u, t.desc.o_cp[u], 4, base + sa(u), base + sa(u) + sn(u) + 1);
-          }
-          for (int u = 1; u < nl; ++u) {
-            const int64_t base = 3 * (h.lv[k0_ + u - 1].off - n1 + sa(u));
-            put(SEG_KI, u, t.desc.o_ki[u], 8, base, base + 3 * sn(u));
-          }
-          for (int u = 0; u + 1 < nl; ++u) {
-            const int64_t lo0 = sa(u) - 2 * sa(u + 1);
-            const int64_t lo1 = (sa(u) + sn(u)) - 2 * (sa(u + 1) + sn(u + 1));
-            const int64_t base = 3 * h.lo_off[k0_ + u - 1];
-            put(SEG_LO, u, t.desc.o_lo[u], 8, base + 3 * lo0, base + 3 * lo1);
-          }
-          if (k0_ > 1) {
-            const int64_t base = h.lv[k0_ - 1].off;
-            put(SEG_N0, 0, t.desc.o_n[0], 8, base + sa(0), base + sa(0) + sn(0));
-          }
-        }
+        t.desc.nseg = 3 * (nl - 1) + (k0_ > 1 ? 1 : 0);
+        const std::vector<int4> segs = make_tile_segs(h, k0_, nl, t.desc, ts, t.ntiles);
         t.segs.alloc(std::max<size_t>(segs.size(), 1));
         MSP_CUDA(cudaMemcpyAsync(t.segs.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
         MSP_CUDA(cudaStreamSynchronize(st));

@@ -29,8 +29,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
+
+#include <nccl.h>
 
 #include "internal.cuh"
 
@@ -524,8 +528,9 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
                                                       double* __restrict__ zpout,
                                                       double* __restrict__ q, double* __restrict__ x,
                                                       double* __restrict__ part, double* __restrict__ scal,
-                                                      unsigned int* __restrict__ cnt) {
-  // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]
+                                                      unsigned int* __restrict__ cnt, int64_t row0, int64_t row1) {
+  // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]; rows
+  // [row0, row1) only (a rank's own rows; all of them on one GPU)
   if ((MSP_EARLY & 16) != 0) pdl_trigger();
   TRACE(0);
 #ifdef MSP_SPMV_PF_PRE  // off since the SpMV launches without PDL (configs[1] 61.7 -> 61.4 us/iteration)
@@ -547,10 +552,11 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   const int64_t nwarps = ((int64_t)gridDim.x * TPB) >> 5;
   double d = 0.0;
   // stage A (slice s): pointers; stage B (slice s): columns, weights, own row
-  int64_t s = warp;
+  const int64_t s_end = (row1 + 31) >> 5;
+  int64_t s = (row0 >> 5) + warp;
   int64_t b0 = 0, b1 = 0;
   if (UNIF) { b0 = s * 32 * MW; b1 = b0 + 32 * MW; }
-  else if (s < nslices) { b0 = sptr[s]; b1 = sptr[s + 1]; }
+  else if (s < s_end) { b0 = sptr[s]; b1 = sptr[s + 1]; }
   int32_t jc[MW];
   double wc[MW];
   double po = 0.0, zr = 0.0;
@@ -574,8 +580,8 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     mk = smask[ss];
     if (r < n) { const double2 v = zp[r]; zr = v.x; po = v.y; }
   };
-  if (s < nslices) load_B(s, b0, b1);
-  while (s < nslices) {
+  if (s < s_end) load_B(s, b0, b1);
+  while (s < s_end) {
     const int64_t s1 = s + nwarps;
 #if MSP_PF_DIST > 0
     if (UNIF && lane == 0) {  // the streams of slice s + PF * nwarps into L2
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
 #endif
     int64_t n0 = 0, n1 = 0;
     if (UNIF) { n0 = s1 * 32 * MW; n1 = n0 + 32 * MW; }
-    else if (s1 < nslices) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
+    else if (s1 < s_end) { n0 = sptr[s1]; n1 = sptr[s1 + 1]; }  // next pointers, in flight
     // current slice: gathers and reduction
     const int wd = UNIF ? MW : (int)((b1 - b0) >> 5);
     const int64_t r = s * 32 + lane;
@@ -606,7 +612,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
 #pragma unroll
     for (int k = 0; k < MW; ++k)
       if (k < wd) acc += wc[k] * (pi - g[k]);
-    if (r < n && !((mk >> lane) & 1u)) {
+    if (r < row1 && r >= row0 && !((mk >> lane) & 1u)) {
       q[r] = acc;
       zpout[2 * r + 1] = pi;
 #ifndef MSP_NO_X_CS
@@ -620,10 +626,11 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     s = s1;
     b0 = n0;
     b1 = n1;
-    if (s < nslices) load_B(s, b0, b1);
+    if (s < s_end) load_B(s, b0, b1);
   }
   for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
     const int64_t r = long_rows[i];
+    if (r < row0 || r >= row1) continue;
     const double2 vr = zp[r];
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
@@ -642,6 +649,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   for (int64_t s = blockIdx.x; s < hd.nseg; s += gridDim.x) {  // CTA per huge-row segment
     const int4 sg = hd.seg[s];
     const int64_t row = long_rows[nlong + sg.x];
+    if (row < row0 || row >= row1) continue;  // block-uniform
     const double2 vr = zp[row];
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
@@ -1598,7 +1606,8 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
 __global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
                                                 const double* __restrict__ yin, double* __restrict__ yout,
                                                 const unsigned int* __restrict__ cnt, int mode_in,
-                                                const int32_t* __restrict__ heavy, int nheavy) {
+                                                const int32_t* __restrict__ heavy, int nheavy, int64_t B0, int64_t nB) {
+  // parents B0 .. B0+nB-1 of level k+1 (a rank's own range; all of them on one GPU)
   // blocks [0, G - nheavy): a thread per aggregate (heavy ones skipped);
   // blocks [G - nheavy, G): a CTA per heavy aggregate
   const int mode = mode_in & 15;
@@ -1607,8 +1616,8 @@ __global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, i
   const int32_t* cp = cptr + lv.cpo[k - 1];
   const int nnorm = (int)gridDim.x - nheavy;
   if ((int)blockIdx.x < nnorm) {
-    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (B < lv.n[k]) {
+    const int64_t B = B0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < B0 + nB) {
       const int32_t c0 = cp[B], c1 = cp[B + 1];
       if (c1 - c0 <= HEAVY_AGG) {
         double y = 0.0;
@@ -1635,8 +1644,10 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
                                                   double* __restrict__ zk, double* __restrict__ wk,
                                                   double* __restrict__ part, double* __restrict__ scal,
                                                   unsigned int* __restrict__ cnt, int mode_in,
-                                                  const int32_t* __restrict__ heavy, int nheavy) {
+                                                  const int32_t* __restrict__ heavy, int nheavy, int64_t B0,
+                                                  int64_t nB) {
   const int mode = mode_in & 15;
+  const bool dist = (mode_in & M_DIST) != 0;
   const int zs = (mode_in & M_ZS2) ? 2 : 1;
   pdl_wait();
   if (mode != M_APPLY && cnt[C_DONE]) return;
@@ -1652,8 +1663,8 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
   };
   const int nnorm = (int)gridDim.x - nheavy;
   if ((int)blockIdx.x < nnorm) {
-    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (B < lv.n[k] && cp[B + 1] - cp[B] <= HEAVY_AGG) {
+    const int64_t B = B0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < B0 + nB && cp[B + 1] - cp[B] <= HEAVY_AGG) {
       const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
       const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
       block_solve(
@@ -1691,7 +1702,11 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
     if (threadIdx.x == 0) part[blockIdx.x] = rz;
     if (mode != M_APPLY && last_block(&cnt[C_DOWN])) {
       const double tot = block_sum_partials<TPB>(part, gridDim.x);
-      if (threadIdx.x == 0) { finish_rz(tot, scal, mode); cnt[C_DOWN] = 0; }
+      if (threadIdx.x == 0) {
+        if (dist) scal[S_RZ] = tot;  // local total: the caller all-reduces
+        else finish_rz(tot, scal, mode);
+        cnt[C_DOWN] = 0;
+      }
     }
   }
 }
@@ -2024,25 +2039,10 @@ struct Prof {
   }
 };
 
-// R r (MSP) on nested vectors.  mode APPLY: r -> z;  INIT / ITER: the PCG
-// step (ITER first updates r) with the scalars of reading R10.
-// ----------------------------------------------------------- multi-GPU
-// State of one rank of the partitioned solve (msp_dist_solve).
-struct DistCtx {
-  msp_comm comm;
-  int64_t row0 = 0, row1 = 0, tile0 = 0, tile1 = 0;
-  int64_t k1 = 0, k1lo = 0, k1hi = 0, k1max = 0;  // first tier's top level, own range, largest range
-  std::vector<int64_t> send_counts, recv_counts;
-  DBuf<int32_t> send_idx, recv_idx;
-  DBuf<double> sendbuf, recvbuf, gbuf_send, gbuf_recv;
-  std::vector<int64_t> k1lo_all;
-};
-
-void comm_check(int rc, const char* what) {
-  if (rc != 0) throw Error{MSP_ERR_CUDA, std::string("communication callback failed: ") + what};
-}
-
+// the scalars of one PCG step after a collective (the steps of a finished
+// solve leave everything, the iteration count included, untouched)
 __global__ void k_dist_finish(int stage, double* scal, unsigned int* cnt, int mode) {
+  if (mode == M_ITER && cnt[C_DONE]) return;
   if (stage == 0) {
     scal[S_ALPHA] = scal[S_RHO] / scal[S_PQ];
   } else if (stage == 1) {
@@ -2052,207 +2052,185 @@ __global__ void k_dist_finish(int stage, double* scal, unsigned int* cnt, int mo
   }
 }
 
-// own rows: x += alpha p_old (deferred), p = z + beta p_old (in place)
-__global__ void k_dist_p(int64_t row0, int64_t row1, const double* __restrict__ z, double* __restrict__ p,
-                         double* __restrict__ x, const double* __restrict__ scal, const unsigned* __restrict__ cnt) {
-  if (cnt[C_DONE]) return;
-  const double beta = scal[S_BETA], alpha = scal[S_ALPHA];
-  for (int64_t i = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row1; i += (int64_t)gridDim.x * blockDim.x) {
-    const double po = p[i];
-    x[i] += alpha * po;
-    p[i] = z[i] + beta * po;
-  }
-}
+// One tier of the sweep schedule as one GPU (or one rank) runs it: the
+// tier's layout and either its tiles (all of them, or a rank's clipped list)
+// or, for a generic tier, the range of parent nodes [B0, B0 + nB) at level
+// k0 + 1 with the heavy aggregates among them.
+struct TierRun {
+  bool generic = false;
+  int k0 = 1, k1 = 1;
+  const TierDesc* desc = nullptr;
+  const int32_t* tstart = nullptr;
+  const int32_t* firstk0 = nullptr;
+  const int4* segs = nullptr;
+  int64_t ntiles = 0;
+  int up_group = 1, tpc = 1;
+  int64_t B0 = 0, nB = 0;
+  const int32_t* heavy = nullptr;
+  int nheavy = 0;
+  size_t smem_up = 0, smem_down = 0;
+};
 
-__global__ void k_take(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ dst) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k < m) dst[k] = src[idx[k]];
-}
-
-__global__ void k_put(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ dst) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k < m) dst[idx[k]] = src[k];
-}
-
-// local (a, b) over [row0, row1) into scal[slot] (fixed order)
-__global__ void __launch_bounds__(TPB) k_dot_rows(int64_t row0, int64_t row1, const double* __restrict__ a,
-                                                  const double* __restrict__ b, double* __restrict__ part,
-                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int slot) {
-  double d = 0.0;
-  for (int64_t i = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row1; i += (int64_t)gridDim.x * blockDim.x)
-    d += a[i] * b[i];
-  d = block_sum<TPB>(d);
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) part[blockIdx.x] = d;
-    if (warp_last_block(&cnt[C_SPMV])) {
-      const double t = warp_sum_partials(part, gridDim.x);
-      if (threadIdx.x == 0) { scal[slot] = t; cnt[C_SPMV] = 0; }
+std::vector<TierRun> tier_runs(Handle& h) {
+  std::vector<TierRun> v;
+  for (auto& T : h.tiers) {
+    TierRun t;
+    t.generic = T.generic;
+    t.k0 = T.k0;
+    t.k1 = T.k1;
+    if (T.generic) {
+      const int k = T.k0;
+      t.B0 = 0;
+      t.nB = h.lv[k].n;
+      t.heavy = h.heavy.p + h.heavy_off[k - 1];
+      t.nheavy = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
+    } else {
+      t.desc = &T.desc;
+      t.tstart = T.tstart.p;
+      t.firstk0 = T.firstk0.p;
+      t.segs = T.segs.p;
+      t.ntiles = T.ntiles;
+      t.up_group = T.up_group;
+      t.tpc = T.desc.tpc;
+      t.smem_up = T.smem_up;
+      t.smem_down = T.smem_down;
     }
+    v.push_back(t);
   }
+  return v;
 }
 
-__global__ void k_pack(int64_t n, const double* __restrict__ src, double* __restrict__ dst, int64_t m) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < m) dst[i] = (i < n) ? src[i] : 0.0;
-}
+enum { PH_UP_LOW = 1, PH_UPPER = 2, PH_DOWN_LOW = 4, PH_ALL = 7 };
 
-bool read_done(Handle& h, cudaStream_t st) {
-  unsigned c[C_NCNT];
-  MSP_CUDA(cudaMemcpyAsync(c, h.counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
-  MSP_CUDA(cudaStreamSynchronize(st));
-  return c[C_DONE] != 0;
-}
-
-// after the first tier's up kernel: all-reduce ((r, r), gdot), convergence
-// test, all-gather y at level k1.  false: converged (stop the sweep).
-bool dist_after_tier1_up(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
-  if (mode != M_APPLY) {
-    comm_check(d.comm.allreduce(h.scal.p + S_RR, 2, d.comm.ctx), "allreduce(rr, gdot)");
-    k_dist_finish<<<1, 1, 0, st>>>(1, h.scal.p, h.counters.p, mode);
-    MSP_LAUNCH_CHECK();
-    h.launches += 1;
-    if (read_done(h, st)) return false;
-  }
-  const int64_t off = h.lv[d.k1 - 1].off;
-  const int64_t m = d.k1max;
-  k_pack<<<grid_for(m), TPB, 0, st>>>(d.k1hi - d.k1lo, h.Y.p + off + d.k1lo, d.gbuf_send.p, m);
-  MSP_LAUNCH_CHECK();
-  comm_check(d.comm.allgather(d.gbuf_send.p, d.gbuf_recv.p, m, d.comm.ctx), "allgather(y_k1)");
-  for (int q = 0; q < d.comm.world; ++q) {
-    const int64_t lo = d.k1lo_all[q], cnt = d.k1lo_all[q + 1] - lo;
-    if (cnt > 0)
-      MSP_CUDA(cudaMemcpyAsync(h.Y.p + off + lo, d.gbuf_recv.p + (int64_t)q * m, cnt * sizeof(double),
-                               cudaMemcpyDeviceToDevice, st));
-  }
-  h.launches += 1;
-  return true;
-}
-
-void dist_after_tier1_down(Handle& h, DistCtx& d, cudaStream_t st, int mode) {
-  if (mode == M_APPLY) return;
-  comm_check(d.comm.allreduce(h.scal.p + S_RZ, 1, d.comm.ctx), "allreduce(rz)");
-  k_dist_finish<<<1, 1, 0, st>>>(2, h.scal.p, h.counters.p, mode);
-  MSP_LAUNCH_CHECK();
-  h.launches += 1;
-}
-
-void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P,
-                DistCtx* dc = nullptr) {
-  const int mbase = mode & 15;
+// R r (MSP) on nested vectors.  mode APPLY: r -> z;  INIT / ITER: the PCG
+// step (ITER first updates r) with the scalars of reading R10.  Tiers
+// 0..tp are the "low" ones (a rank's own part when distributed: M_DIST makes
+// their reductions rank-local totals, and the levels above run replicated);
+// `phases` selects the up sweep of the low tiers, everything above them
+// (upper tiers, coarse levels), and the down sweep of the low tiers.
+void msp_sweeps_runs(Handle& h, const Lv& lv, const std::vector<TierRun>& runs, int tp, const double* q, double* r,
+                     double* z, cudaStream_t st, int mode, Prof& P, int phases) {
   double* part_rr = h.red.p;                  // [cap/4]
   double* part_rz = h.red.p + h.red_cap / 4;
   double* part_gd = h.red.p + h.red_cap / 2;
   unsigned* cnt = h.counters.p;
   double* scal = h.scal.p;
-  const int nt = (int)h.tiers.size();
-  const int npart_up = (int)((h.tiers[0].ntiles + h.tiers[0].up_group - 1) / h.tiers[0].up_group);
-  // ---- up
-  for (int i = 0; i < nt; ++i) {
-    auto& T = h.tiers[i];
+  const int nt = (int)runs.size();
+  const bool dist = (mode & M_DIST) != 0;
+  const int npart_up = runs.empty() || runs[0].generic ? 0 : (int)((runs[0].ntiles + runs[0].up_group - 1) / runs[0].up_group);
+  auto up = [&](int i) {
+    const TierRun& T = runs[i];
+    const int md = (i <= tp) ? mode : (mode & ~M_DIST);
     P.begin();
     if (T.generic) {
       const int k = T.k0;
       const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
-      const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
-      launch_c(16, k_up_lvl, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, yin,
-             h.Y.p + h.lv[k].off, (const unsigned*)cnt, mode, (const int32_t*)(h.heavy.p + h.heavy_off[k - 1]), nh);
+      launch_c(16, k_up_lvl, grid_for(std::max<int64_t>(T.nB, 1)) + T.nheavy, TPB, 0, st, lv, k,
+               (const int32_t*)h.cptr.p, yin, h.Y.p + h.lv[k].off, (const unsigned*)cnt, md, T.heavy, T.nheavy, T.B0,
+               T.nB);
       P.end(PC_MID_UP);
     } else {
+      const unsigned grid = (unsigned)std::max<int64_t>(1, (T.ntiles + T.up_group - 1) / T.up_group);
       if (T.k0 == 1)
-        launch_c(4, k_tile_up<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.up_group - 1) / T.up_group), UT,
-               T.smem_up, st, lv,
-               T.desc, (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p,
-               h.Y.p, part_rr, part_gd, scal, cnt, mode | (dc ? M_DIST : 0), (int)(dc ? dc->tile0 : 0));
+        launch_c(4, k_tile_up<true>, grid, UT, T.smem_up, st, lv, *T.desc, T.tstart, T.firstk0, q, r,
+                 (const double*)h.Hvec.p, h.Y.p, part_rr, part_gd, scal, cnt, md, 0);
       else
-        launch_c(4, k_tile_up<false>, (unsigned)((T.ntiles + T.up_group - 1) / T.up_group), UT, T.smem_up, st, lv, T.desc,
-               (const int32_t*)T.tstart.p, (const int32_t*)T.firstk0.p, q, r, (const double*)h.Hvec.p, h.Y.p,
-               part_rr, part_gd, scal, cnt, mode, 0);
+        launch_c(4, k_tile_up<false>, grid, UT, T.smem_up, st, lv, *T.desc, T.tstart, T.firstk0, q, r,
+                 (const double*)h.Hvec.p, h.Y.p, part_rr, part_gd, scal, cnt, md & ~M_DIST, 0);
       P.end(T.k0 == 1 ? PC_TILE_UP : PC_MID_UP);
     }
     ++h.launches;
-    if (dc && i == 0 && !dist_after_tier1_up(h, *dc, st, mbase)) return;  // converged
-  }
-  // ---- coarse (folded into the top tier's down kernel in GEMV mode, and
-  // into the last tier's down kernel when merged)
-  const bool merged = h.merged_coff > 0 && !dc;
-  if (!h.gemv && !merged) {
-    P.begin();
-    const double* y0 = (h.Kc == 1) ? r : h.Y.p;
-    launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p,
-           (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p,
-           y0, h.Z.p, h.W.p, z, (const double*)part_gd, npart_up, scal, cnt, mode | (dc ? M_DIST : 0),
-           (const double*)h.Mtop.p);
-    P.end(PC_COARSE);
-    ++h.launches;
-  }
-  // ---- down
-  for (int i = nt - 1; i >= 0; --i) {
-    auto& T = h.tiers[i];
-    if (!T.generic && T.k1 == T.k0) continue;  // the (1,1) update-only tier
+  };
+  const bool merged = h.merged_coff > 0 && (!dist || tp < nt - 1);
+  auto down = [&](int i) {
+    const TierRun& T = runs[i];
+    if (!T.generic && T.k1 == T.k0) return;  // the (1,1) update-only tier
+    const int md = (i <= tp) ? mode : (mode & ~M_DIST);
     P.begin();
     if (T.generic) {
       const int k = T.k0;
       const int64_t ok = h.lv[k - 1].off, op = h.lv[k].off;
-      const int nh = (int)(h.heavy_off[k] - h.heavy_off[k - 1]);
-      const int32_t* hv = h.heavy.p + h.heavy_off[k - 1];
+      const unsigned grid = grid_for(std::max<int64_t>(T.nB, 1)) + T.nheavy;
       if (k == 1)
-        launch_c(16, k_down_lvl<true>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
-               (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p,
-               (const double*)(h.Z.p + op), (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt,
-               mode, hv, nh);
+        launch_c(16, k_down_lvl<true>, grid, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+                 (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p, (const double*)(h.Z.p + op),
+                 (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt, md, T.heavy, T.nheavy, T.B0,
+                 T.nB);
       else
-        launch_c(16, k_down_lvl<false>, grid_for(h.lv[k].n) + nh, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p,
-               (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)(h.Y.p + ok),
-               (const double*)h.Nsub.p, (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok,
-               h.W.p + ok, part_rz, scal, cnt, mode, hv, nh);
+        launch_c(16, k_down_lvl<false>, grid, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+                 (const double*)h.lof.p, (const double*)(h.Y.p + ok), (const double*)h.Nsub.p,
+                 (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok, h.W.p + ok, part_rz, scal,
+                 cnt, md & ~M_DIST, T.heavy, T.nheavy, T.B0, T.nB);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1)
-        launch_c(8, k_tile_down<true>, (unsigned)(dc ? dc->tile1 - dc->tile0 : (T.ntiles + T.desc.tpc - 1) / T.desc.tpc),
-               TT, T.smem_down, st, lv,
-               T.desc,
-               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
-               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
-               cnt, mode | (dc ? M_DIST : 0), (const double*)h.Mco.p, (const double*)part_gd, npart_up,
-               (const double*)h.Y.p, (int)(dc ? dc->tile0 : 0), (const int4*)T.segs.p, h.cdesc, 0,
-               (const double*)nullptr, (const double*)nullptr);
+        launch_c(8, k_tile_down<true>, (unsigned)std::max<int64_t>(1, (T.ntiles + T.tpc - 1) / T.tpc), TT,
+                 T.smem_down, st, lv, *T.desc, T.tstart, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+                 (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
+                 cnt, md, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0, T.segs,
+                 h.cdesc, 0, (const double*)nullptr, (const double*)nullptr);
       else if (merged && i == nt - 1)  // the coarse levels run inside this kernel
-        launch_c(8, k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, T.desc,
-               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
-               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
-               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
-               (const int4*)T.segs.p, h.cdesc, (int)h.merged_coff, (const double*)h.top_pinv.p,
-               (const double*)h.Mtop.p);
+        launch_c(8, k_tile_down<false, true>, (unsigned)T.ntiles, CT, h.merged_smem, st, lv, *T.desc, T.tstart,
+                 (const int32_t*)h.cptr.p, (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)h.Nsub.p,
+                 (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz, scal, cnt, md & ~M_DIST, (const double*)h.Mco.p,
+                 (const double*)part_gd, npart_up, (const double*)h.Y.p, 0, T.segs, h.cdesc, (int)h.merged_coff,
+                 (const double*)h.top_pinv.p, (const double*)h.Mtop.p);
       else
-        launch_c(8, k_tile_down<false>, (unsigned)T.ntiles, TT, T.smem_down, st, lv, T.desc,
-               (const int32_t*)T.tstart.p, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
-               (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz,
-               scal, cnt, mode, (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0,
-               (const int4*)T.segs.p, h.cdesc, 0, (const double*)nullptr, (const double*)nullptr);
+        launch_c(8, k_tile_down<false>, (unsigned)std::max<int64_t>(1, T.ntiles), TT, T.smem_down, st, lv, *T.desc,
+                 T.tstart, (const int32_t*)h.cptr.p, (const double*)h.kinv.p, (const double*)h.lof.p,
+                 (const double*)h.Nsub.p, (const double*)h.Y.p, h.Z.p, h.W.p, z, part_rz, scal, cnt, md & ~M_DIST,
+                 (const double*)h.Mco.p, (const double*)part_gd, npart_up, (const double*)h.Y.p, 0, T.segs, h.cdesc,
+                 0, (const double*)nullptr, (const double*)nullptr);
       P.end(T.k0 == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     }
     ++h.launches;
+  };
+  if (phases & PH_UP_LOW)
+    for (int i = 0; i <= tp && i < nt; ++i) up(i);
+  if (phases & PH_UPPER) {
+    for (int i = tp + 1; i < nt; ++i) up(i);
+    // coarse (folded into the top tier's down kernel in GEMV mode, and into
+    // the last tier's down kernel when merged)
+    if (!h.gemv && !merged) {
+      P.begin();
+      const double* y0 = (h.Kc == 1) ? r : h.Y.p;
+      launch(k_coarse, 1u, CT, h.coarse_smem, st, lv, h.cdesc, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
+             (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)h.top_pinv.p, y0, h.Z.p, h.W.p, z,
+             (const double*)part_gd, npart_up, scal, cnt, mode, (const double*)h.Mtop.p);
+      P.end(PC_COARSE);
+      ++h.launches;
+    }
+    for (int i = nt - 1; i > tp; --i) down(i);
   }
-  if (dc) dist_after_tier1_down(h, *dc, st, mbase);
+  if (phases & PH_DOWN_LOW)
+    for (int i = std::min(tp, nt - 1); i >= 0; --i) down(i);
+}
+
+void msp_sweeps(Handle& h, const Lv& lv, const double* q, double* r, double* z, cudaStream_t st, int mode, Prof& P) {
+  const std::vector<TierRun> runs = tier_runs(h);
+  msp_sweeps_runs(h, lv, runs, (int)runs.size() - 1, q, r, z, st, mode, P, PH_ALL);
 }
 
 template <bool PCG>
 void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
-                 cudaStream_t st) {
+                 cudaStream_t st, int64_t row0 = 0, int64_t row1 = -1) {
+  if (row1 < 0) row1 = h.n;
   launch_c(1, k_spmv<PCG>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
          (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
          (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
-         (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, (int64_t)0, h.n);
+         (const double*)h.w1.p, z, pold, pnew, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1);
   ++h.launches;
 }
 
 // SpMV of the MSP iteration on interleaved (z, p) pairs (M_ZS2)
-void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st) {
+void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st,
+                       int64_t row0 = 0, int64_t row1 = -1) {
+  if (row1 < 0) row1 = h.n;
   auto go = [&](auto kern) {
     launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
            (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(), (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
-           reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p);
+           reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1);
   };
   if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true>);
@@ -2650,140 +2628,7 @@ extern "C" int msp_debug_phase(unsigned long long* out, int reset) {
 namespace msp {
 
 // One rank of the partitioned PCG-MSP solve (msp_dist_solve), nested vectors.
-void pcg_dist_nested(Handle& h, const msp_comm& comm, const double* b, double* x, double rtol, int maxit,
-                     cudaStream_t st, msp_report* rep) {
-  if (h.tiers.empty() || h.tiers[0].generic || h.tiers[0].k1 < 2 || h.Kc < 2)
-    throw Error{MSP_ERR_UNSUPPORTED, "multi-GPU solve needs a tiled first tier (graph too small or too irregular)"};
-  const Handle::Tier& T1 = h.tiers[0];
-  DistCtx d;
-  d.comm = comm;
-  const int W = comm.world, R = comm.rank;
-  // ---- plan (host): level-1 CSR and first-tier tile starts to the host
-  std::vector<int32_t> rp(h.n + 1), cl(h.nnz_adj), ts((size_t)(T1.k1 - T1.k0 + 1) * (T1.ntiles + 1));
-  MSP_CUDA(cudaMemcpy(rp.data(), h.rowptr1.p, rp.size() * 4, cudaMemcpyDeviceToHost));
-  MSP_CUDA(cudaMemcpy(cl.data(), h.col1.p, cl.size() * 4, cudaMemcpyDeviceToHost));
-  MSP_CUDA(cudaMemcpy(ts.data(), T1.tstart.p, ts.size() * 4, cudaMemcpyDeviceToHost));
-  const int64_t nt1 = T1.ntiles + 1;
-  int64_t range[4];
-  d.send_counts.assign(W, 0);
-  d.recv_counts.assign(W, 0);
-  int rc = msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, R, range, d.recv_counts.data(),
-                              d.send_counts.data(), nullptr, 0, nullptr, 0);
-  if (rc) throw Error{rc, "partition plan"};
-  int64_t nrecv = 0, nsend = 0;
-  for (int q = 0; q < W; ++q) { nrecv += d.recv_counts[q]; nsend += d.send_counts[q]; }
-  std::vector<int64_t> rr(std::max<int64_t>(nrecv, 1)), sr(std::max<int64_t>(nsend, 1));
-  rc = msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, R, range, d.recv_counts.data(),
-                          d.send_counts.data(), rr.data(), nrecv, sr.data(), nsend);
-  if (rc) throw Error{rc, "partition plan"};
-  d.row0 = range[0]; d.row1 = range[1]; d.tile0 = range[2]; d.tile1 = range[3];
-  d.k1 = T1.k1;
-  const int64_t top = (int64_t)(T1.k1 - T1.k0) * nt1;
-  d.k1lo_all.assign(W + 1, 0);
-  for (int q = 0; q <= W; ++q) {
-    // rank q's tile range, recomputed with the same rule
-    int64_t rq[4];
-    std::vector<int64_t> dummy(W);
-    if (q < W) {
-      msp_partition_plan(h.n, rp.data(), cl.data(), T1.ntiles, ts.data(), W, q, rq, dummy.data(), dummy.data(),
-                         nullptr, 0, nullptr, 0);
-      d.k1lo_all[q] = ts[top + rq[2]];
-    } else {
-      d.k1lo_all[q] = ts[top + T1.ntiles];
-    }
-  }
-  d.k1lo = d.k1lo_all[R];
-  d.k1hi = d.k1lo_all[R + 1];
-  d.k1max = 1;
-  for (int q = 0; q < W; ++q) d.k1max = std::max<int64_t>(d.k1max, d.k1lo_all[q + 1] - d.k1lo_all[q]);
-  std::vector<int32_t> si(sr.begin(), sr.begin() + std::max<int64_t>(nsend, 1)), ri(rr.begin(), rr.begin() + std::max<int64_t>(nrecv, 1));
-  d.send_idx.alloc(si.size()); d.recv_idx.alloc(ri.size());
-  MSP_CUDA(cudaMemcpy(d.send_idx.p, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
-  MSP_CUDA(cudaMemcpy(d.recv_idx.p, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice));
-  d.sendbuf.alloc(std::max<int64_t>(nsend, 1)); d.recvbuf.alloc(std::max<int64_t>(nrecv, 1));
-  d.gbuf_send.alloc(d.k1max); d.gbuf_recv.alloc(d.k1max * W);
-
-  const int64_t n = h.n;
-  const Lv lv = make_level_table(h);
-  cudaEvent_t e0, e1;
-  MSP_CUDA(cudaEventCreate(&e0));
-  MSP_CUDA(cudaEventCreate(&e1));
-  const int64_t launches0 = h.launches;
-  MSP_CUDA(cudaEventRecord(e0, st));
-  MSP_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), st));
-  MSP_CUDA(cudaMemcpyAsync(h.vr.p, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  MSP_CUDA(cudaMemsetAsync(h.vp.p, 0, n * sizeof(double), st));
-  launch(k_init_state, 1u, 1u, 0, st, h.scal.p, h.counters.p, rtol * rtol);
-  Prof P(h, st);
-  msp_sweeps(h, lv, nullptr, h.vr.p, h.vz.p, st, M_INIT, P, &d);
-  const unsigned gr = std::min<unsigned>(grid_for(std::max<int64_t>(d.row1 - d.row0, 1)), 148u * 4u);
-  int it = 0;
-  bool done = read_done(h, st);
-  while (!done && it < maxit) {
-    // p = z + beta p (own rows), halo exchange of p, q = L p, (p, q)
-    k_dist_p<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vz.p, h.vp.p, x, h.scal.p, h.counters.p);
-    if (nsend) k_take<<<grid_for(nsend), TPB, 0, st>>>(nsend, d.send_idx.p, h.vp.p, d.sendbuf.p);
-    MSP_LAUNCH_CHECK();
-    comm_check(d.comm.alltoallv(d.sendbuf.p, d.send_counts.data(), d.recvbuf.p, d.recv_counts.data(), d.comm.ctx),
-               "alltoallv(p halo)");
-    if (nrecv) k_put<<<grid_for(nrecv), TPB, 0, st>>>(nrecv, d.recv_idx.p, d.recvbuf.p, h.vp.p);
-    launch(k_spmv<false>, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p,
-           (const int32_t*)h.sell_col.p, (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
-           (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p,
-           (const double*)h.w1.p, (const double*)h.vp.p, (const double*)nullptr, (double*)nullptr, h.vq.p,
-           (double*)nullptr, h.red.p, h.scal.p, h.counters.p, d.row0, d.row1);
-    k_dot_rows<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vp.p, h.vq.p, h.red.p, h.scal.p, h.counters.p, (int)S_PQ);
-    MSP_LAUNCH_CHECK();
-    comm_check(d.comm.allreduce(h.scal.p + S_PQ, 1, d.comm.ctx), "allreduce(pq)");
-    k_dist_finish<<<1, 1, 0, st>>>(0, h.scal.p, h.counters.p, M_ITER);
-    h.launches += 6;
-    // r -= alpha q, (r, r), z = R r, (r, z)
-    msp_sweeps(h, lv, h.vq.p, h.vr.p, h.vz.p, st, M_ITER, P, &d);
-    ++it;
-    done = read_done(h, st);
-  }
-  // x += alpha p for the last direction (own rows)
-  {
-    unsigned c[C_NCNT];
-    MSP_CUDA(cudaMemcpyAsync(c, h.counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
-    MSP_CUDA(cudaStreamSynchronize(st));
-    if (c[C_IT] > 0) {
-      MSP_CUDA(cudaMemsetAsync(h.counters.p + C_DONE, 0, sizeof(unsigned), st));
-      k_dist_p<<<gr, TPB, 0, st>>>(d.row0, d.row1, h.vz.p, h.vp.p, x, h.scal.p, h.counters.p);
-      MSP_LAUNCH_CHECK();
-      if (c[C_DONE]) MSP_CUDA(cudaMemcpyAsync(h.counters.p + C_DONE, &c[C_DONE], sizeof(unsigned), cudaMemcpyHostToDevice, st));
-    }
-  }
-  MSP_CUDA(cudaEventRecord(e1, st));
-  MSP_CUDA(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  MSP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  double hs[S_NSCAL];
-  unsigned hc[C_NCNT];
-  MSP_CUDA(cudaMemcpy(hs, h.scal.p, sizeof(hs), cudaMemcpyDeviceToHost));
-  MSP_CUDA(cudaMemcpy(hc, h.counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
-  if (rep) {
-    rep->iterations = (int32_t)hc[C_IT];
-    rep->converged = hc[C_DONE] ? 1 : 0;
-    rep->relres = hs[S_BB] > 0 ? std::sqrt(hs[S_RR] / hs[S_BB]) : 0.0;
-    rep->solve_ms = ms;
-    rep->kernel_launches = h.launches - launches0;
-  }
-  h.dist_row0 = d.row0;
-  h.dist_row1 = d.row1;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-}
-
-__global__ void k_zero_outside(int64_t n, int64_t r0, int64_t r1, double* __restrict__ x) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n && (i < r0 || i >= r1)) x[i] = 0.0;
-}
-
-void zero_outside(Handle& h, double* x, cudaStream_t st) {
-  k_zero_outside<<<grid_for(h.n), TPB, 0, st>>>(h.n, h.dist_row0, h.dist_row1, x);
-  MSP_LAUNCH_CHECK();
-}
+#include "dist_solve.cuh"
 
 }  // namespace msp
 

@@ -1,12 +1,17 @@
-"""Multi-GPU binding: the collectives msp_dist_solve calls back into, over
-torch.distributed (NCCL on GPUs, gloo on CPU for tests), and the host-only
-partition plan.  Marshalling only -- the solve runs in libmsp_b200.so.
+"""Multi-GPU binding of libmsp_b200.so (marshalling only -- the partition,
+the collectives (NCCL, inside the library) and the solve run in the C ABI).
 
     import torch.distributed as dist
     from paper_2207_07847_b200 import setup
-    from paper_2207_07847_b200.dist import TorchComm, dist_solve
-    S = setup(n, rowptr, col, w)                     # every rank, full graph
-    out = dist_solve(S, TorchComm(), b, rtol=1e-8)   # x: own rows, 0 elsewhere
+    from paper_2207_07847_b200.dist import dist_init, dist_solve
+    S = setup(n, rowptr, col, w)            # every rank, full graph, same seed
+    dist_init(S)                            # NCCL communicator from torch.distributed's group
+    out = dist_solve(S, b, rtol=1e-8)       # x: own rows, 0 elsewhere
+
+``group_solve`` runs the same decomposition for W ranks in ONE process on one
+device (loopback collectives): the single-GPU test of the partitioned
+arithmetic.  ``boundaries`` and ``halo_plan`` are the host-only plan steps
+(CPU tests).
 """
 from __future__ import annotations
 
@@ -16,128 +21,101 @@ import numpy as np
 
 from . import _lib as L
 
-
-class msp_comm(ctypes.Structure):
-    pass
-
-
-ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
-ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
-ALLTOALLV = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p,
-                             ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
-msp_comm._fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("allreduce", ALLREDUCE),
-                     ("allgather", ALLGATHER), ("alltoallv", ALLTOALLV), ("ctx", ctypes.c_void_p)]
+P = ctypes.c_void_p
+i32, i64 = ctypes.c_int32, ctypes.c_int64
 
 
-class _CAI:
-    """Zero-copy view of n fp64 at a CUDA device pointer (__cuda_array_interface__)."""
-
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
-                                         "version": 3, "strides": None}
-
-
-def _view(ptr: int, n: int, device):
-    import torch
-    if n == 0:
-        return torch.empty(0, dtype=torch.float64, device=device)
-    if device.type == "cuda":
-        return torch.as_tensor(_CAI(ptr, n), device=device)
-    buf = (ctypes.c_double * int(n)).from_address(int(ptr))
-    return torch.from_numpy(np.frombuffer(buf, dtype=np.float64))
+def _f(name, argtypes):
+    f = getattr(L._lib, name)
+    f.argtypes = argtypes
+    f.restype = ctypes.c_int
+    return f
 
 
-class TorchComm:
-    """msp_comm callbacks over a torch.distributed process group.  Buffers
-    are device pointers (CUDA) or host pointers when `device` is CPU."""
-
-    def __init__(self, group=None, device=None):
-        import torch
-        import torch.distributed as dist
-        self.dist = dist
-        self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        if device is None:
-            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
-                else torch.device("cpu")
-        self.device = torch.device(device)
-        self._cb = (ALLREDUCE(self._allreduce), ALLGATHER(self._allgather), ALLTOALLV(self._alltoallv))
-        self.c = msp_comm(self.world, self.rank, self._cb[0], self._cb[1], self._cb[2], None)
-        self.error = None
-
-    def _guard(self, f):
-        try:
-            f()
-            return 0
-        except Exception as e:  # reported through the C error path
-            self.error = e
-            return -1
-
-    def _allreduce(self, ptr, n, ctx):
-        return self._guard(lambda: self.dist.all_reduce(_view(ptr, n, self.device), group=self.group))
-
-    def _allgather(self, sptr, rptr, n_each, ctx):
-        def f():
-            s = _view(sptr, n_each, self.device)
-            r = _view(rptr, n_each * self.world, self.device)
-            self.dist.all_gather_into_tensor(r, s, group=self.group)
-        return self._guard(f)
-
-    def _alltoallv(self, sptr, scounts, rptr, rcounts, ctx):
-        def f():
-            sc = [int(scounts[q]) for q in range(self.world)]
-            rc = [int(rcounts[q]) for q in range(self.world)]
-            s = _view(sptr, sum(sc), self.device)
-            r = _view(rptr, sum(rc), self.device)
-            self.dist.all_to_all_single(r, s, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
-        return self._guard(f)
+def unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    L._check(_f("msp_dist_unique_id", [P])(buf))
+    return buf.raw
 
 
-def partition_plan(n, rowptr, col, tile_rows, world: int, rank: int):
-    """msp_partition_plan (host only): (range, recv_counts, send_counts,
-    recv_rows, send_rows) of `rank` for the CSR (rowptr, col) whose first-tier
-    tiles start at tile_rows."""
-    lib = L._lib
+def dist_init(solver, group=None, stream=None) -> np.ndarray:
+    """msp_dist_init for this rank of torch.distributed's (default) group:
+    rank 0's NCCL unique id is broadcast through torch.distributed.  Returns
+    msp_dist_range (row0, row1, kp, tp, nsend, nrecv, world, rank)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    obj = [unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    idb = ctypes.create_string_buffer(obj[0], 128)
+    L._check(_f("msp_dist_init", [P, i32, i32, P, P])(solver._h, world, rank, idb, L._stream_ptr(stream)))
+    return dist_range(solver)
+
+
+def dist_range(solver) -> np.ndarray:
+    out = np.zeros(8, dtype=np.int64)
+    L._check(_f("msp_dist_range", [P, P])(solver._h, out.ctypes.data))
+    return out
+
+
+def dist_solve(solver, b, x=None, rtol: float = 1e-8, maxit: int = 100000, stream=None) -> dict:
+    """msp_dist_solve on this rank (collective over the ranks)."""
+    x = L._like(b) if x is None else x
+    pb, mb, _ = L._ptr_mem(b, np.float64)
+    px, mx, _ = L._ptr_mem(x, np.float64)
+    if mb != mx:
+        raise ValueError("b and x must live in the same memory space")
+    rep = L._Report()
+    f = _f("msp_dist_solve", [P, P, P, ctypes.c_double, i32, ctypes.c_int, P, ctypes.POINTER(L._Report)])
+    L._check(f(solver._h, pb, px, float(rtol), int(maxit), mb, L._stream_ptr(stream), ctypes.byref(rep)))
+    out = {f_: getattr(rep, f_) for f_, _ in L._Report._fields_}
+    out["x"] = x
+    return out
+
+
+def group_solve(solvers, b, x=None, rtol: float = 1e-8, maxit: int = 100000, stream=None) -> dict:
+    """msp_dist_group_solve: len(solvers) ranks (each a setup of the same
+    graph) driven by this process on one device; x is the assembled
+    solution."""
+    W = len(solvers)
+    x = L._like(b) if x is None else x
+    pb, mb, _ = L._ptr_mem(b, np.float64)
+    px, mx, _ = L._ptr_mem(x, np.float64)
+    if mb != mx:
+        raise ValueError("b and x must live in the same memory space")
+    hs = (P * W)(*[s._h for s in solvers])
+    rep = L._Report()
+    f = _f("msp_dist_group_solve", [ctypes.POINTER(P), i32, P, P, ctypes.c_double, i32, ctypes.c_int, P,
+                                    ctypes.POINTER(L._Report)])
+    L._check(f(hs, W, pb, px, float(rtol), int(maxit), mb, L._stream_ptr(stream), ctypes.byref(rep)))
+    out = {f_: getattr(rep, f_) for f_, _ in L._Report._fields_}
+    out["x"] = x
+    return out
+
+
+def boundaries(cost, world: int) -> np.ndarray:
+    """msp_dist_boundaries (host only): quantile split of the prefix cost."""
+    cost = np.ascontiguousarray(cost, dtype=np.int64)
+    bnd = np.zeros(world + 1, dtype=np.int64)
+    L._check(_f("msp_dist_boundaries", [i64, P, i32, P])(int(cost.size - 1), cost.ctypes.data, int(world),
+                                                           bnd.ctypes.data))
+    return bnd
+
+
+def halo_plan(n, rowptr, col, row_bnd, rank: int):
+    """msp_halo_plan (host only): (recv_counts, send_counts, recv_rows,
+    send_rows) of `rank` given level-1 row boundaries."""
     rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
     col = np.ascontiguousarray(col, dtype=np.int32)
-    tile_rows = np.ascontiguousarray(tile_rows, dtype=np.int32)
-    rng = np.zeros(4, dtype=np.int64)
+    row_bnd = np.ascontiguousarray(row_bnd, dtype=np.int64)
+    world = row_bnd.size - 1
     rc = np.zeros(world, dtype=np.int64)
     sc = np.zeros(world, dtype=np.int64)
-    P = ctypes.c_void_p
-    f = lib.msp_partition_plan
-    f.argtypes = [ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P,
-                  ctypes.c_int64, P, ctypes.c_int64]
-    f.restype = ctypes.c_int
-    args = (int(n), rowptr.ctypes.data, col.ctypes.data, int(tile_rows.size - 1), tile_rows.ctypes.data,
-            int(world), int(rank), rng.ctypes.data, rc.ctypes.data, sc.ctypes.data)
+    f = _f("msp_halo_plan", [i64, P, P, i32, P, i32, P, P, P, i64, P, i64])
+    args = (int(n), rowptr.ctypes.data, col.ctypes.data, int(world), row_bnd.ctypes.data, int(rank),
+            rc.ctypes.data, sc.ctypes.data)
     L._check(f(*args, None, 0, None, 0))
     rr = np.zeros(max(int(rc.sum()), 1), dtype=np.int64)
     sr = np.zeros(max(int(sc.sum()), 1), dtype=np.int64)
     L._check(f(*args, rr.ctypes.data, int(rc.sum()), sr.ctypes.data, int(sc.sum())))
-    return rng, rc, sc, rr[:int(rc.sum())], sr[:int(sc.sum())]
-
-
-def dist_solve(solver, comm: TorchComm, b, x=None, rtol: float = 1e-8, maxit: int = 100000, stream=None) -> dict:
-    """msp_dist_solve on this rank (collective: every rank of comm calls it)."""
-    lib = L._lib
-    x = L._like(b) if x is None else x
-    pb, mb, kb = L._ptr_mem(b, np.float64)
-    px, mx, kx = L._ptr_mem(x, np.float64)
-    if mb != mx:
-        raise ValueError("b and x must live in the same memory space")
-    rep = L._Report()
-    f = lib.msp_dist_solve
-    f.argtypes = [ctypes.c_void_p, ctypes.POINTER(msp_comm), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
-                  ctypes.c_int32, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(L._Report)]
-    f.restype = ctypes.c_int
-    rc = f(solver._h, ctypes.byref(comm.c), pb, px, float(rtol), int(maxit), mb, L._stream_ptr(stream),
-           ctypes.byref(rep))
-    if comm.error is not None:
-        e, comm.error = comm.error, None
-        raise RuntimeError(f"communication callback failed: {e}")
-    L._check(rc)
-    out = {f_: getattr(rep, f_) for f_, _ in L._Report._fields_}
-    out["x"] = x
-    return out
+    return rc, sc, rr[:int(rc.sum())], sr[:int(sc.sum())]

@@ -1,7 +1,9 @@
-"""Multi-GPU host logic on the CPU (no GPU): the partition / halo plan of
-msp_partition_plan and the torch.distributed callbacks of dist.TorchComm,
-exercised by world-size-2 gloo processes that emulate the distributed SpMV
-(own rows + exchanged halo) and check it against the global product."""
+"""Multi-GPU host logic on the CPU (no GPU): the partition boundaries
+(msp_dist_boundaries) and the halo plan (msp_halo_plan) of the partitioned
+solve, and a world-size-2 gloo run in which each process knows only its own
+rows, exchanges the planned halo through torch.distributed, and reproduces
+the global SpMV on its rows exactly -- the data-path step the NCCL send/recv
+of msp_dist_solve performs on GPUs."""
 import os
 import socket
 
@@ -25,10 +27,6 @@ def _lib_ok():
 pytestmark = pytest.mark.skipif(not _lib_ok(), reason="libmsp_b200.so does not build here")
 
 
-def tiles_of(n, T):
-    return np.array(sorted(set(list(range(0, n, T)) + [n])), dtype=np.int32)
-
-
 def laplacian_apply(g, x, rows):
     y = np.zeros(rows.size)
     for k, i in enumerate(rows):
@@ -38,31 +36,47 @@ def laplacian_apply(g, x, rows):
     return y
 
 
+def row_bounds(g, world):
+    """Rows split by the solve's cost rule (entries + 8 per row), at row level."""
+    from paper_2207_07847_b200.dist import boundaries
+    cost = g.rowptr.astype(np.int64) + 8 * np.arange(g.n + 1)
+    return boundaries(cost, world)
+
+
+def test_boundaries_balance_and_cover():
+    from paper_2207_07847_b200.dist import boundaries
+    rng = np.random.default_rng(0)
+    cost = np.concatenate([[0], np.cumsum(rng.integers(1, 50, 1000))])
+    for W in (1, 2, 3, 8):
+        b = boundaries(cost, W)
+        assert b[0] == 0 and b[-1] == 1000 and np.all(np.diff(b) > 0)
+        share = np.diff(cost[b])
+        assert share.max() - share.min() <= 2 * 49 + 1          # within one node of the quantiles
+    # a rank that would own nothing: every rank gets MSP_ERR_UNSUPPORTED
+    from paper_2207_07847_b200 import _lib as L
+    with pytest.raises(L.MspError) as ei:
+        boundaries(np.arange(4), 5)
+    assert ei.value.code == -4
+
+
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
-def test_plan_partitions_rows_and_halos_are_symmetric(world):
-    from paper_2207_07847_b200.dist import partition_plan
+def test_halo_plan_is_symmetric_and_exact(world):
+    from paper_2207_07847_b200.dist import halo_plan
     g = G.rgg(700, 12.0, 4)
-    tr = tiles_of(g.n, 37)
-    plans = [partition_plan(g.n, g.rowptr, g.col, tr, world, r) for r in range(world)]
-    starts = [int(p[0][0]) for p in plans] + [g.n]
-    assert starts[0] == 0 and all(int(plans[r][0][1]) == starts[r + 1] for r in range(world))
-    for r, (rng, rc, sc, rr, sr) in enumerate(plans):
-        r0, r1, t0, t1 = (int(v) for v in rng)
-        assert tr[t0] == r0 and tr[t1] == r1          # whole tiles
-        own = np.arange(r0, r1)
+    rb = row_bounds(g, world)
+    plans = [halo_plan(g.n, g.rowptr, g.col, rb, r) for r in range(world)]
+    for r, (rc, sc, rr, sr) in enumerate(plans):
+        r0, r1 = rb[r], rb[r + 1]
         nb = set()
-        for i in own:
+        for i in range(r0, r1):
             nb.update(int(c) for c in g.col[g.rowptr[i]:g.rowptr[i + 1]] if not (r0 <= c < r1))
         assert sorted(nb) == list(rr)                  # exactly the outside neighbours
-        assert rc.sum() == rr.size and sc.sum() == sr.size
-    # what r sends to q is what q receives from r
-    for r in range(world):
-        soff = np.concatenate([[0], np.cumsum(plans[r][2])])
+        assert rc.sum() == rr.size and sc.sum() == sr.size and rc[r] == 0 and sc[r] == 0
+    for r in range(world):                             # what r sends to q is what q receives from r
+        soff = np.concatenate([[0], np.cumsum(plans[r][1])])
         for q in range(world):
-            sent = plans[r][4][soff[q]:soff[q + 1]]
-            roff = np.concatenate([[0], np.cumsum(plans[q][1])])
-            got = plans[q][3][roff[r]:roff[r + 1]]
-            assert np.array_equal(sent, got), (r, q)
+            roff = np.concatenate([[0], np.cumsum(plans[q][0])])
+            assert np.array_equal(plans[r][3][soff[q]:soff[q + 1]], plans[q][2][roff[r]:roff[r + 1]]), (r, q)
 
 
 def _worker(rank, world, port, q):
@@ -70,36 +84,21 @@ def _worker(rank, world, port, q):
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        from paper_2207_07847_b200.dist import TorchComm, partition_plan
-        comm = TorchComm(device="cpu")
-        g = G.grid2d(23, 17, "loguniform", 2)
-        tr = tiles_of(g.n, 29)
-        rng, rc, sc, rr, sr = partition_plan(g.n, g.rowptr, g.col, tr, world, rank)
-        r0, r1 = int(rng[0]), int(rng[1])
-        p = np.random.default_rng(5).standard_normal(g.n)  # same on all ranks (the reference)
-        mine = np.zeros(g.n)
-        mine[r0:r1] = p[r0:r1]                              # a rank only knows its own rows
-        send = np.ascontiguousarray(mine[sr])
-        recv = np.zeros(max(rr.size, 1))
-        rcc = np.ascontiguousarray(rc, dtype=np.int64)
-        scc = np.ascontiguousarray(sc, dtype=np.int64)
-        PI = ctypes_ptr = None  # noqa: F841
-        import ctypes
-        ok = comm._alltoallv(send.ctypes.data, scc.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                             recv.ctypes.data, rcc.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), None)
-        assert ok == 0, comm.error
-        mine[rr] = recv[:rr.size]
-        y_own = laplacian_apply(g, mine, np.arange(r0, r1))
-        y_ref = laplacian_apply(g, p, np.arange(r0, r1))
-        assert np.array_equal(y_own, y_ref)
-        # all-reduce and all-gather callbacks
-        v = np.array([float(rank + 1), 2.0])
-        assert comm._allreduce(v.ctypes.data, 2, None) == 0
-        assert v[0] == world * (world + 1) / 2 and v[1] == 2.0 * world
-        s = np.full(3, float(rank))
-        out = np.zeros(3 * world)
-        assert comm._allgather(s.ctypes.data, out.ctypes.data, 3, None) == 0
-        assert np.array_equal(out, np.repeat(np.arange(world, dtype=float), 3))
+        from paper_2207_07847_b200.dist import halo_plan
+        for g in (G.grid2d(23, 17, "loguniform", 2), G.chung_lu(3000, 2.1, 16.0, 1)):
+            rb = row_bounds(g, world)
+            rc, sc, rr, sr = halo_plan(g.n, g.rowptr, g.col, rb, rank)
+            r0, r1 = int(rb[rank]), int(rb[rank + 1])
+            p = np.random.default_rng(5).standard_normal(g.n)  # the reference (same on all ranks)
+            mine = np.zeros(g.n)
+            mine[r0:r1] = p[r0:r1]                              # a rank only knows its own rows
+            send = torch.from_numpy(np.ascontiguousarray(mine[sr]))
+            recv = torch.zeros(int(rr.size), dtype=torch.float64)
+            dist.all_to_all_single(recv, send, output_split_sizes=[int(c) for c in rc],
+                                   input_split_sizes=[int(c) for c in sc])
+            mine[rr] = recv.numpy()
+            rows = np.arange(r0, r1)
+            assert np.array_equal(laplacian_apply(g, mine, rows), laplacian_apply(g, p, rows))
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
@@ -120,17 +119,3 @@ def test_gloo_world2_halo_exchange_reproduces_global_spmv():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
-
-
-def test_plan_rejects_rank_without_tiles():
-    """More ranks than tiles: every rank gets MSP_ERR_UNSUPPORTED from the
-    plan (a deterministic check on shared inputs, so all ranks fail together
-    before any collective instead of one hanging)."""
-    from paper_2207_07847_b200 import _lib as L
-    from paper_2207_07847_b200.dist import partition_plan
-    g = G.grid2d(6, 5)
-    tr = tiles_of(g.n, 16)                       # 2 tiles
-    for r in range(3):
-        with pytest.raises(L.MspError) as ei:
-            partition_plan(g.n, g.rowptr, g.col, tr, 3, r)
-        assert ei.value.code == -4
