@@ -13,10 +13,11 @@ ones); --config 1 / 3 give the 2D 1024^2 grid and the 4M-point random
 geometric graph.  value = nnz(L_G) x iterations x (ranks) / seconds.
 Setup (GPU hierarchy + expansion + MSP) is timed separately (setup_ms).
 
-Multi-GPU (torchrun, N > 1): each rank solves its own instance of the
-workload (independent problems, no data-path collective) -> "scaling":
-"weak"; timing is the max over ranks.  The row-partitioned single-graph path
-is a §8 "next" row.
+Multi-GPU (torchrun, N > 1): the ranks solve ONE system together through
+msp_dist_solve (row partition, NCCL halo exchange / all-reduces / all-gather
+inside the library) -> "scaling": "strong"; timing is the max over ranks.
+--replicas gives the old one-problem-per-rank mode ("weak"); --dist runs the
+partitioned path at N = 1 too.
 
 --impl reference times the oracle (oracle/, plain fp64 CPU, test
 infrastructure) on the host cores on a bounded sample of the same workload.
@@ -195,21 +196,25 @@ class OracleWorkload:
     def sample(self, seconds: float, cores: int = 1):
         """PCG-MSP iterations for about `seconds` on `cores` processes:
         (aggregate nnz*iters/s, total iterations, wall seconds, cores)."""
-        if self.one is None:
-            it, dt = self._iters(2)
-            self.one = max(dt / 2, 1e-4)
-        iters = max(2, int(seconds / self.one))
         if cores <= 1:
-            it, dt = self._iters(iters)
+            if self.one is None:
+                it, dt = self._iters(2)
+                self.one = max(dt / 2, 1e-4)
+            it, dt = self._iters(max(2, int(seconds / self.one)))
             return self.g.nnz_laplacian * it / dt, it, dt, 1
         import multiprocessing as mp
         global _WL
         _WL = self
         ctx = mp.get_context("fork")          # children share the factorisation
-        t = time.time()
         with ctx.Pool(cores) as pool:
+            if self.one is None:               # per-iteration time with every core busy
+                t = time.time()
+                pool.map(_sample_child, [3] * cores)
+                self.one = max((time.time() - t) / 3, 1e-4)
+            iters = max(2, int(seconds / self.one))
+            t = time.time()
             res = pool.map(_sample_child, [iters] * cores)
-        wall = time.time() - t
+            wall = time.time() - t
         tot = sum(r[0] for r in res)
         return self.g.nnz_laplacian * tot / wall, tot, wall, cores
 
@@ -247,8 +252,8 @@ def run_reference(args, rank):
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / len(vals),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args, wl.g),
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_dict(args, wl.g),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{vals[0][1]} iterations per step in total; " + wl.describe(args.config)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -257,19 +262,26 @@ def run_reference(args, rank):
     return 0
 
 
-def config_dict(args, g, extra=None):
+def config_dict(args, g, extra=None, parallelism=None):
     names = {0: "2D grid 32x32, uniform[1,10] weights", 1: "2D grid 1024x1024, log-uniform[1e-3,1e3] weights",
              2: "3D 7-point anisotropic grid 256^3", 3: "random geometric graph 4M points",
-             4: "Chung-Lu power-law 50M vertices"}
+             4: "Chung-Lu power-law 50M vertices (largest component)"}
     d = {"workload": f"BASELINE configs[{args.config}]: {names.get(args.config, '?')}; PCG+{args.precond.upper()} "
                      f"to rtol {args.rtol:g}",
          "n": g.n if g is not None else None, "nnz_L": g.nnz_laplacian if g is not None else None,
          "precond": args.precond, "mu": args.mu, "rtol": args.rtol, "levels": "max",
-         "parallelism": f"independent problem per rank x{args.gpus}",
+         "parallelism": parallelism or f"independent problem per rank x{args.gpus}",
          "l2": "flushed (256 MiB write) before every timed step, inside the timed region"}
     if extra:
         d.update(extra)
     return d
+
+
+class GraphInfo:
+    def __init__(self, n, nnz_adj):
+        self.n = int(n)
+        self.nnz_adj = int(nnz_adj)
+        self.nnz_laplacian = self.nnz_adj + self.n
 
 
 # ------------------------------------------------------------ our arm
@@ -284,6 +296,10 @@ def main():
     ap.add_argument("--mu", type=float, default=0.8)
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=200000)
+    ap.add_argument("--dist", action="store_true",
+                    help="row-partitioned solve (msp_dist_solve) even at one GPU; the default for N > 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent problem per rank instead of one partitioned problem")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -293,25 +309,53 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank)
 
+    # stdout carries exactly one JSON line: keep NCCL's banner off it
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     import torch
     import torch.distributed as dist
-    from inputs import graphs as G
+    from inputs import device as D, graphs as G
     import paper_2207_07847_b200 as M
+    from paper_2207_07847_b200 import dist as MD
 
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    use_dist = (world > 1 and not args.replicas) or args.dist
+    if use_dist and args.precond != "msp":
+        raise SystemExit("the partitioned solve is PCG-MSP")
+    if use_dist and world == 1 and not dist.is_initialized():
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
 
-    g = G.config_graph(args.config, seed=0)
-    b_np = G.rhs(g.n, 0)
     t0 = time.time()
-    S = M.setup(g.n, torch.as_tensor(g.rowptr, device=dev), torch.as_tensor(g.col, device=dev),
-                torch.as_tensor(g.val, device=dev), mu=args.mu, seed=0)
+    n, rp, col, val = D.config_csr(args.config, 1.0, 0, dev)
+    g = GraphInfo(n, int(rp[-1].item()))
+    b_np = G.rhs(g.n, 0)
+    log(f"graph n={g.n} nnz(L)={g.nnz_laplacian} in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    S = M.setup(n, rp, col, val, mu=args.mu, seed=0)
+    del rp, col, val
     info = S.info()
     log(f"setup {info['setup_ms']:.1f} ms (wall {time.time() - t0:.1f}s) levels={info['levels']} "
         f"n~={info['n_tilde']} mwm_rounds={info['mwm_rounds']}")
+    drange = None
+    if use_dist:
+        drange = MD.dist_init(S)
+        log(f"partition: rows [{drange[0]}, {drange[1]}) kp={drange[2]} tp={drange[3]} "
+            f"halo send={drange[4]} recv={drange[5]}")
+
+    def solve(b_, x_):
+        if use_dist:
+            return MD.dist_solve(S, b_, x_, rtol=args.rtol, maxit=args.maxit)
+        return S.pcg_solve(b_, x_, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+
     b = torch.as_tensor(b_np, device=dev)
     x = torch.empty_like(b)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -319,7 +363,7 @@ def main():
 
     for _ in range(args.warmup):
         flush.fill_(1.0)
-        rep = S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+        rep = solve(b, x)
     log(f"warmup: {rep['iterations']} iterations, converged={rep['converged']}, "
         f"{rep['solve_ms']:.1f} ms")
 
@@ -335,7 +379,7 @@ def main():
     iters, launches = [], 0
     for _ in range(args.steps):
         flush.fill_(1.0)
-        rep = S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+        rep = solve(b, x)
         iters.append(rep["iterations"])
         launches += rep["kernel_launches"] + 1
     ev1.record(stream)
@@ -350,18 +394,22 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     it = int(np.median(iters))
-    value = world * g.nnz_laplacian * sum(iters) / (ms_total / 1000.0)
+    # partitioned: all ranks solve ONE system (strong scaling); replicas: one each (weak)
+    copies = 1 if use_dist else world
+    value = copies * g.nnz_laplacian * sum(iters) / (ms_total / 1000.0)
 
     # ---- e2e: same metric through the C ABI with host buffers (pinned)
     bh = torch.as_tensor(b_np).pin_memory()
     xh = torch.empty_like(bh).pin_memory()
-    S.pcg_solve(bh, xh, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+    solve(bh, xh)
     torch.cuda.synchronize()
     e_iters = []
+    if world > 1:
+        dist.barrier()
     te = time.perf_counter()
     for _ in range(max(1, min(args.steps, 3))):
         flush.fill_(1.0)
-        r2 = S.pcg_solve(bh, xh, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+        r2 = solve(bh, xh)
         e_iters.append(r2["iterations"])
     torch.cuda.synchronize()
     te = time.perf_counter() - te
@@ -369,22 +417,25 @@ def main():
         t = torch.tensor([te], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
-    e2e_value = world * g.nnz_laplacian * sum(e_iters) / te
+    e2e_value = copies * g.nnz_laplacian * sum(e_iters) / te
 
-    # ---- profiled replay of one step: per-kernel device time (CUDA events)
+    # ---- profiled replay of one step: per-kernel device time (CUDA events
+    # bracketing each launch on the solve's stream; serialised, no graph)
     S.set_profiling(True)
     flush.fill_(1.0)
-    S.pcg_solve(b, x, rtol=args.rtol, maxit=args.maxit, precond=args.precond)
+    solve(b, x)
     S.set_profiling(False)
     prof = S.get_profile()
     sizes = S.level_sizes()
-    n2 = int(sizes[1]) if len(sizes) > 1 else 0
-    nnz_adj = int(g.rowptr[-1])
     sz = [int(v) for v in sizes]
     kt = int(info["tile_level"])
-    model = {"spmv": spmv_bytes(g.n, nnz_adj), "tile_up": tile_up_bytes(sz, kt)}
+    n_own = g.n if not use_dist else int(drange[1] - drange[0])
+    nnz_own = g.nnz_adj if not use_dist else int(round(g.nnz_adj * n_own / g.n))
+    model = {"spmv": spmv_bytes(n_own, nnz_own), "tile_up": tile_up_bytes(sz, kt)}
     if kt >= 2:
         model["tile_down"] = tile_down_bytes(sz, kt)
+    if use_dist and world > 1:  # the tile byte models are whole-graph figures
+        model = {"spmv": model["spmv"]}
     hbm, peak_src = measured_peaks()
     breakdown = {}
     for k, v in prof.items():
@@ -421,14 +472,21 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "oracle", "sample": f"failed: {ex}"}
 
     if rank == 0:
+        par = (f"row-partitioned x{world} (msp_dist_solve: NCCL halo / all-reduce / all-gather)" if use_dist
+               else f"independent problem per rank x{world}")
+        extra = {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"]),
+                 "tile_level": int(info["tile_level"]), "coarse_level": int(info["coarse_level"]),
+                 "ntiles": int(info["ntiles"]), "ntiers": int(info["ntiers"])}
+        if use_dist:
+            extra["partition_level"] = int(drange[2])
+            extra["rank0_rows"] = int(drange[1] - drange[0])
+            extra["rank0_halo"] = {"send": int(drange[4]), "recv": int(drange[5])}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if use_dist else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, g, {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"]),
-                                             "tile_level": int(info["tile_level"]),
-                                             "coarse_level": int(info["coarse_level"]),
-                                             "ntiles": int(info["ntiles"]), "ntiers": int(info["ntiers"])}),
+            "config": config_dict(args, g, extra, par),
             "iterations": it, "time_to_rtol_s": ms_step / 1000.0, "setup_ms": info["setup_ms"],
             "solve_GBps_algorithmic": round(whole_gbps, 1) if whole_gbps else None,
             "roofline": roofline, "kernel_breakdown": breakdown,
@@ -439,7 +497,7 @@ def main():
             "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

@@ -268,8 +268,25 @@ DistRank* dist_build(Handle& h, int world, int rank, const void* id128, cudaStre
     }
     TierDesc ds = T.desc;
     ds.ntiles = (int)ntr;
-    ds.up_group = 1;  // the up kernel's layout was sized for its own grouping; clipped tiles are smaller
-    ds.tpc = 1;
+    // the up kernel's grouping of consecutive tiles, its layout re-sized for
+    // the clipped tiles; the down kernel's tiles per CTA as on one GPU
+    const int G = T.up_group;
+    {
+      auto a16 = [](int64_t b) { return (int)((b + 15) & ~(int64_t)15); };
+      int64_t c0 = 0, c1 = 0;
+      for (int64_t j = 0; j < ntr; j += G) {
+        const int64_t je = std::min<int64_t>(j + G, ntr);
+        c0 = std::max<int64_t>(c0, (int64_t)rts[je] - rts[j]);
+        c1 = std::max<int64_t>(c1, (int64_t)rts[(size_t)(nl - 1) * (ntr + 1) + je] - rts[(size_t)(nl - 1) * (ntr + 1) + j]);
+      }
+      ds.o_uf = 0;
+      ds.o_uy0 = a16((c1 + 1 + 8) * 4);
+      ds.o_uq = a16(ds.o_uy0 + (c0 + 2) * 8);
+      ds.o_uh = a16(ds.o_uq + (c0 + 2) * 8);
+      ds.smem_up = (T.k0 == 1) ? a16(ds.o_uh + (c0 + 2) * 8) : a16(ds.o_uy0 + (c0 + 2) * 8);
+      ds.up_group = G;
+      raise_smem_limit(T.k0 == 1 ? (const void*)k_tile_up<true> : (const void*)k_tile_up<false>, ds.smem_up);
+    }
     d->descs[t] = ds;
     d->tstarts[t].alloc(rts.size());
     MSP_CUDA(cudaMemcpyAsync(d->tstarts[t].p, rts.data(), rts.size() * 4, cudaMemcpyHostToDevice, st));
@@ -283,8 +300,9 @@ DistRank* dist_build(Handle& h, int world, int rank, const void* id128, cudaStre
     R.tstart = d->tstarts[t].p;
     R.segs = nl > 1 ? d->segs[t].p : nullptr;
     R.ntiles = ntr;
-    R.up_group = 1;
-    R.tpc = 1;
+    R.up_group = G;
+    R.tpc = ds.tpc;
+    R.smem_up = ds.smem_up;
   }
   MSP_CUDA(cudaStreamSynchronize(st));
   // halo plan (host, from the level-1 nested CSR)

@@ -768,9 +768,9 @@ __global__ void __launch_bounds__(UT) k_tile_up(const __grid_constant__ Lv lv, c
   __shared__ int sa0, sn0, sa1, sn1, skf, sky0, sdone, skr, skq, skh;
   __shared__ double salpha;
   // this CTA's tiles [tA, tB): `group` consecutive tiles (1 when distributed)
-  const int grp = (mode_in & M_DIST) ? 1 : td.up_group;
+  const int grp = td.up_group;
   const int tA = tile0 + blockIdx.x * grp, tB = min(tA + grp, td.ntiles);
-  const int tile = (mode_in & M_DIST) ? tA : blockIdx.x;  // partial-sum slot
+  const int tile = blockIdx.x;  // partial-sum slot
   const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // early trigger (MSP_EARLY bit 1: tier >= 2 up, bit 2: first-tier up): the
@@ -1249,7 +1249,7 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   const int nl = td.nl, k0 = td.k0, nt1 = td.ntiles + 1;
   // first tier (not distributed): tpc consecutive tiles per CTA, one after
   // another (the block reduction and ticket once per CTA)
-  const int tpc = (FIRST && !COARSE && !(mode_in & M_DIST) && td.tpc > 1) ? td.tpc : 1;
+  const int tpc = (FIRST && !COARSE && td.tpc > 1) ? td.tpc : 1;
   const int tid = threadIdx.x;
   const int64_t n1 = lv.n[0];
   if ((COARSE ? (MSP_EARLY & 4) : FIRST ? (MSP_EARLY & 8) : (MSP_EARLY & 4)) != 0) pdl_trigger();
