@@ -191,20 +191,18 @@ def test_cg_unpreconditioned_small():
     assert abs(out["iterations"] - ref.iterations) <= 2
 
 
-@pytest.mark.parametrize("mu", [0.5, 0.3, pytest.param(None, marks=pytest.mark.xfail(
-    strict=True, reason="mu = 1/sqrt(n): R r is conditioned ~1e15 (R8 at this mu, DESIGN.md R8/R14); "
-                        "the fp64 block-tree apply is 0.19 off the exact value (mpmath-checked reference)"))])
+@pytest.mark.parametrize("mu", [0.5, 0.3, None])
 def test_apply_R_other_mu(mu):
     """Below the practical mu = 0.8 the T~ weights span mu^{2(l-1)}: the
     same 1e-12 bar against the refined reference (R14), met at
-    0.5 and 0.3; at mu = 1/sqrt(n) (7 levels, weights down to 1e-15) no
-    fp64 elimination resolves R r -- a documented limit, not a claim."""
+    0.5, 0.3 and mu = 1/sqrt(n) (7 levels, weights down to ~1e-15; the
+    refined reference agrees with a 50-digit mpmath solve to 4e-16 there,
+    tools/mp_check_mu.py)."""
     g = G.grid2d(20, 13, "loguniform", 7)
     mu = 1 / np.sqrt(g.n) if mu is None else mu
     h = A.build_hierarchy(g, 2)
     s = gpu_setup(g, mu, 0, 2)
     sysm = E.expand_msp_only(g, h, mu)
-    R = PR.msp(sysm)
     r = G.rhs(g.n, 9)
     apply_R_bar(f"grid20x13_mu{mu:.3f}", s.apply_R(dt(r)).cpu().numpy(), sysm, r)
 

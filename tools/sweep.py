@@ -16,12 +16,12 @@ CHILD = r"""
 import json, sys, torch
 sys.path.insert(0, %r)
 import paper_2207_07847_b200 as M
-from inputs import graphs as G
+from inputs import graphs as G, device as D
 dev = torch.device('cuda:0')
-g = G.config_graph(%d)
-S = M.setup(g.n, torch.as_tensor(g.rowptr, device=dev), torch.as_tensor(g.col, device=dev),
-            torch.as_tensor(g.val, device=dev), mu=0.8)
-b = torch.as_tensor(G.rhs(g.n, 0), device=dev); x = torch.empty_like(b)
+n, rp, col, val = D.config_csr(%d, %r, 0, dev)
+S = M.setup(n, rp, col, val, mu=0.8)
+del rp, col, val
+b = torch.as_tensor(G.rhs(n, 0), device=dev); x = torch.empty_like(b)
 S.pcg_solve(b, x, rtol=0.0, maxit=200)
 rs = [S.pcg_solve(b, x, rtol=0.0, maxit=%d) for _ in range(3)]
 ms = min(r['solve_ms'] for r in rs)
@@ -35,6 +35,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=2000)
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("settings", nargs="*")
     a = ap.parse_args()
     for st in (a.settings or [""]):
@@ -49,7 +50,7 @@ def main():
                 env["MSP_LIB_OVERRIDE"] = path
             else:
                 env[k] = v
-        r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.config, a.iters)], env=env,
+        r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.config, a.scale, a.iters)], env=env,
                            capture_output=True, text=True, timeout=600)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
         print(f"[{st}] {line}", flush=True)
