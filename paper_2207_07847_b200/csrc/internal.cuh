@@ -159,6 +159,11 @@ struct Handle {
     int up_group = 1;         // tiles per CTA of the up kernel
   };
   std::vector<Tier> tiers;
+  // first tier's down sweep by k_wtile_down (a warp per tile): grid and
+  // per-warp shared-memory region
+  bool wdown = false;
+  unsigned wdown_grid = 0;
+  int wdown_region = 0;
   int32_t Kc = 1;
   size_t coarse_smem = 0;
   CoarseDesc cdesc{};

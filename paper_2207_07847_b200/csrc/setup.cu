@@ -1102,6 +1102,10 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
   }
 
   clk.mark(st, "top pseudo-inverse");
+  {
+    const char* e = std::getenv("MSP_WDOWN");
+    h.wdown = e ? std::atoi(e) != 0 : false;
+  }
   build_schedule(h, st);
   clk.mark(st, "schedule");
   MSP_CUDA(cudaEventRecord(e1, st));
@@ -1261,6 +1265,12 @@ void build_schedule(Handle& h, cudaStream_t st) {
   if (const char* e = std::getenv("MSP_TILE_T")) T = std::max<int64_t>(16, std::atoll(e));
   SUB = T / 2;
   if (const char* e = std::getenv("MSP_TILE_SUB")) SUB = std::max<int64_t>(2, std::atoll(e));
+  // the first tier's tiles and subtree cap (its down kernel runs a warp per
+  // tile, k_wtile_down: smaller tiles, more independent warps per SM)
+  int64_t T1 = T, SUB1 = SUB;
+  if (h.wdown) { T1 = 128; SUB1 = 128; }
+  if (const char* e = std::getenv("MSP_WTILE")) T1 = std::max<int64_t>(16, std::atoll(e));
+  if (const char* e = std::getenv("MSP_WSUB")) SUB1 = std::max<int64_t>(2, std::atoll(e));
   if (const char* e = std::getenv("MSP_COARSE_MAX")) CMAX = std::max<int64_t>(2, std::atoll(e));
   const size_t SMEM_CAP = 200 * 1024;
   const Lv lv = make_level_table(h);
@@ -1290,12 +1300,14 @@ void build_schedule(Handle& h, cudaStream_t st) {
   // tiers over levels 1..Kc
   h.tiers.clear();
   int k0 = 1;
+  const int64_t T0 = T;
   auto add_tiles = [&](int k0_, int k1_, DBuf<int32_t>* first_k1) {
     Handle::Tier t;
     t.k0 = k0_;
     t.k1 = k1_;
     const int nl = k1_ - k0_ + 1;
     const int64_t n0 = h.lv[k0_ - 1].n;
+    const int64_t T = (k0_ == 1) ? T1 : T0;
     t.ntiles = std::max<int64_t>(1, (n0 + T - 1) / T);
     const int64_t nt1 = t.ntiles + 1;
     t.tstart.alloc((size_t)nl * nt1);
@@ -1405,7 +1417,7 @@ void build_schedule(Handle& h, cudaStream_t st) {
     MSP_CUDA(cudaStreamSynchronize(st));
     int k1 = k0;
     for (int k = k0 + 1; k <= kmax; ++k) {
-      if (maxsz[k - k0] <= SUB) k1 = k;
+      if (maxsz[k - k0] <= (k0 == 1 ? SUB1 : SUB)) k1 = k;
       else break;
     }
     if (k1 == k0) {  // an aggregate with more than SUB children: one generic level

@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 // column / weight / row vectors of s+1 are already in flight.
 #undef TRACE_KID
 #define TRACE_KID 6
-template <int MW, bool UNIF>
+template <int MW, bool UNIF, bool SEP = false>
 __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
                                                       const uint32_t* __restrict__ smask, int64_t nlong, const HugeDesc hd,
@@ -528,9 +528,21 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
                                                       double* __restrict__ zpout,
                                                       double* __restrict__ q, double* __restrict__ x,
                                                       double* __restrict__ part, double* __restrict__ scal,
-                                                      unsigned int* __restrict__ cnt, int64_t row0, int64_t row1) {
-  // zp[i] = (z_i, p_old_i); the new p_i goes to zpout[2 i + 1]; rows
+                                                      unsigned int* __restrict__ cnt, int64_t row0, int64_t row1,
+                                                      const double* __restrict__ zs, const double* __restrict__ ps,
+                                                      double* __restrict__ pn) {
+  // pairs (!SEP): zp[i] = (z_i, p_old_i), the new p_i goes to zpout[2 i + 1];
+  // SEP: z, p_old and the new p in three plain vectors zs, ps, pn (every
+  // store a full sector: no L2 fill of a half-written pair line).  Rows
   // [row0, row1) only (a rank's own rows; all of them on one GPU)
+  auto zpj = [&](int64_t j) -> double2 {
+    if (SEP) return make_double2(zs[j], ps[j]);
+    return zp[j];
+  };
+  auto put_p = [&](int64_t r, double v) {
+    if (SEP) pn[r] = v;
+    else zpout[2 * r + 1] = v;
+  };
   if ((MSP_EARLY & 16) != 0) pdl_trigger();
   TRACE(0);
 #ifdef MSP_SPMV_PF_PRE  // off since the SpMV launches without PDL (configs[1] 61.7 -> 61.4 us/iteration)
@@ -578,7 +590,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
       }
     }
     mk = smask[ss];
-    if (r < n) { const double2 v = zp[r]; zr = v.x; po = v.y; }
+    if (r < n) { const double2 v = zpj(r); zr = v.x; po = v.y; }
   };
   if (s < s_end) load_B(s, b0, b1);
   while (s < s_end) {
@@ -589,7 +601,12 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
       if ((sp + 1) * 32 <= n) {
         l2_prefetch(scol + sp * 32 * MW, 32 * MW * 4);
         l2_prefetch(sw + sp * 32 * MW, 32 * MW * 8);
-        l2_prefetch(zp + sp * 32, 32 * 16);
+        if (SEP) {
+          l2_prefetch(zs + sp * 32, 32 * 8);
+          l2_prefetch(ps + sp * 32, 32 * 8);
+        } else {
+          l2_prefetch(zp + sp * 32, 32 * 16);
+        }
         l2_prefetch(x + sp * 32, 32 * 8);
       }
     }
@@ -605,7 +622,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
 #pragma unroll
     for (int k = 0; k < MW; ++k)
       if (k < wd) {
-        const double2 v = zp[jc[k]];
+        const double2 v = zpj(jc[k]);
         g[k] = v.x + beta * v.y;
       }
     double acc = 0.0;
@@ -614,7 +631,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
       if (k < wd) acc += wc[k] * (pi - g[k]);
     if (r < row1 && r >= row0 && !((mk >> lane) & 1u)) {
       q[r] = acc;
-      zpout[2 * r + 1] = pi;
+      put_p(r, pi);
 #ifndef MSP_NO_X_CS
       __stcs(x + r, __ldcs(x + r) + alpha * po);
 #else
@@ -631,17 +648,17 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
     const int64_t r = long_rows[i];
     if (r < row0 || r >= row1) continue;
-    const double2 vr = zp[r];
+    const double2 vr = zpj(r);
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
     double acc = row_dot<32>(col, w, rowptr[r], rowptr[r + 1], lane, pi, [&](int32_t j) {
-      const double2 v = zp[j];
+      const double2 v = zpj(j);
       return v.x + beta * v.y;
     });
     acc = warp_sum(acc);
     if (lane == 0) {
       q[r] = acc;
-      zpout[2 * r + 1] = pi;
+      put_p(r, pi);
       x[r] += alpha * pr;
       d += pi * acc;
     }
@@ -650,18 +667,18 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     const int4 sg = hd.seg[s];
     const int64_t row = long_rows[nlong + sg.x];
     if (row < row0 || row >= row1) continue;  // block-uniform
-    const double2 vr = zp[row];
+    const double2 vr = zpj(row);
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
     double acc = row_dot<TPB>(col, w, sg.y, sg.z, threadIdx.x, pi, [&](int32_t j) {
-      const double2 v = zp[j];
+      const double2 v = zpj(j);
       return v.x + beta * v.y;
     });
     acc = block_sum<TPB>(acc);
     double tot;
     if (threadIdx.x == 0 && huge_last(hd, sg.x, s, acc, &tot)) {
       q[row] = tot;
-      zpout[2 * row + 1] = pi;
+      put_p(row, pi);
       x[row] += alpha * pr;
       d += pi * tot;
     }
@@ -924,6 +941,98 @@ __global__ void __launch_bounds__(UT) k_tile_up(const __grid_constant__ Lv lv, c
   if (threadIdx.x == 0) atomicAdd(&g_phase[TRACE_KID][15], 1ull);
 #endif
   TRACE_END();
+}
+
+// ------------------------------------------------- first-tier up, streamed
+// The first tier's up sweep as a plain stream (no staging): FG lanes per
+// level-k1 node, each lane loading r, q, H of four of the node's level-1
+// descendants at a time straight from global memory, so every lane keeps 12
+// independent loads in flight and the grid (a few CTAs per SM, striding over
+// the nodes) stays balanced.  Per node: r -= alpha q (mode ITER), the node's
+// sum y_k1; per CTA: (r, r) and gdot = (H, r) partials, last-CTA ticket.
+// FLAT: a level-1-only tier (no y), one element per lane and step.
+template <bool FLAT>
+__global__ void __launch_bounds__(UT) k_up_stream(int64_t nnodes, const int32_t* __restrict__ f, int64_t n1,
+                                                  const double* __restrict__ q, double* __restrict__ r,
+                                                  const double* __restrict__ H, double* __restrict__ yk1,
+                                                  double* __restrict__ part_rr, double* __restrict__ part_gd,
+                                                  double* __restrict__ scal, unsigned int* __restrict__ cnt, int mode) {
+  constexpr int FG = MSP_FLAT_G;
+  constexpr int U = 4;  // elements per lane in flight
+  mode &= 15;
+  const int sub = threadIdx.x & (FG - 1);
+  const int64_t base0 = (int64_t)blockIdx.x * (UT / FG);
+  pdl_wait();
+  if (mode == M_ITER && cnt[C_DONE]) return;  // uniform
+  const double alpha = (mode == M_ITER) ? scal[S_ALPHA] : 0.0;
+  const bool upd = (mode == M_ITER);
+  double rr = 0.0, gd = 0.0;
+  auto elem = [&](int64_t c, double rv, double qv, double hv, double& y) {
+    double ri = rv;
+    if (upd) {
+      ri -= alpha * qv;
+      r[c] = ri;
+    }
+    rr += ri * ri;
+    gd += hv * ri;
+    y += ri;
+  };
+  if (FLAT) {
+    const int64_t T = (int64_t)gridDim.x * UT;
+    double y = 0.0;
+    for (int64_t c0 = (int64_t)blockIdx.x * UT + threadIdx.x; c0 < n1; c0 += U * T) {
+      double rv[U], qv[U], hv[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t c = c0 + k * T;
+        if (c < n1) { rv[k] = r[c]; qv[k] = upd ? __ldcs(q + c) : 0.0; hv[k] = H[c]; }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t c = c0 + k * T;
+        if (c < n1) elem(c, rv[k], qv[k], hv[k], y);
+      }
+    }
+  } else {
+    const int64_t ngrp = (int64_t)gridDim.x * UT / FG;
+    // block-uniform trip count (the groups of a warp shuffle together)
+    for (int64_t b = base0; b < nnodes; b += ngrp) {
+      const int64_t i = b + (threadIdx.x / FG);
+      double y = 0.0;
+      if (i < nnodes) {
+        const int64_t e0 = f[i], e1 = f[i + 1];
+        for (int64_t c0 = e0 + sub; c0 < e1; c0 += U * FG) {
+          double rv[U], qv[U], hv[U];
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int64_t c = c0 + k * FG;
+            if (c < e1) { rv[k] = r[c]; qv[k] = upd ? __ldcs(q + c) : 0.0; hv[k] = H[c]; }
+          }
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int64_t c = c0 + k * FG;
+            if (c < e1) elem(c, rv[k], qv[k], hv[k], y);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = FG / 2; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (sub == 0 && i < nnodes) yk1[i] = y;
+    }
+  }
+  pdl_trigger();
+  const double2 v = block_sum2<UT>(make_double2(rr, gd));
+  if (threadIdx.x < 32) {  // only warp 0 waits on the ticket
+    if (threadIdx.x == 0) { part_rr[blockIdx.x] = v.x; part_gd[blockIdx.x] = v.y; }
+    if (mode != M_APPLY && warp_last_block(&cnt[C_UPD])) {
+      const double2 t2 = warp_sum_partials2(part_rr, part_gd, gridDim.x);
+      if (threadIdx.x == 0) {
+        scal[S_GD] = t2.y;
+        finish_rr(t2.x, scal, cnt, mode);
+        cnt[C_UPD] = 0;
+      }
+    }
+  }
 }
 
 // --------------------------------------------------------- coarse kernel
@@ -1598,6 +1707,238 @@ __global__ void __launch_bounds__(COARSE ? CT : TT) k_tile_down(const __grid_con
   TRACE_END();
 }
 
+// ------------------------------------------------- first-tier down, per warp
+// The first tier's down sweep with one warp per tile (tiles of ~MSP_WTILE
+// level-1 nodes): every warp stages its own tile with TMA bulk copies onto
+// its own mbarrier and runs the tile's levels with __syncwarp between them,
+// so the warps of an SM are independent chains (no CTA barrier per level)
+// and the next tile's copies of one warp overlap the other warps' compute.
+// Same arithmetic, in the same order, as k_tile_down<true> (its header and
+// DESIGN.md "MSP apply"): recompute y, N of levels 2 .. k1-1, then the block
+// solves down to level 1, whose output w_1 = R r goes to zout (stride zs)
+// with (r, R r) accumulated.
+#ifndef MSP_WD
+#define MSP_WD 4
+#endif
+constexpr int WD = MSP_WD;  // warps per CTA
+__global__ void __launch_bounds__(WD * 32) k_wtile_down(const __grid_constant__ Lv lv, const __grid_constant__ TierDesc td,
+                                                       const int32_t* __restrict__ tstart,
+                                                       const int32_t* __restrict__ cptr, const double* __restrict__ kinv,
+                                                       const double* __restrict__ lof, const double* __restrict__ rin,
+                                                       const double* __restrict__ Zg, const double* __restrict__ Wg,
+                                                       double* __restrict__ zout, double* __restrict__ part,
+                                                       double* __restrict__ scal, unsigned int* __restrict__ cnt,
+                                                       int mode_in, const int4* __restrict__ segs, int region) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bars[WD];
+  __shared__ LvlPtr tbs[WD][MAXT];
+  __shared__ int ssa[WD][MAXT], ssn[WD][MAXT], skc_[WD][MAXT], skk_[WD][MAXT], skl_[WD][MAXT], skd[WD][4];
+  const int mode = mode_in & 15;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  char* sm = smem + (size_t)wid * region;
+  uint64_t* bar = &bars[wid];
+  LvlPtr* tb = tbs[wid];
+  int* sa = ssa[wid];
+  int* sn = ssn[wid];
+  const int nl = td.nl, nt1 = td.ntiles + 1, m1 = nl - 1;
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  const int zs = (mode_in & M_ZS2) ? 2 : 1;
+  const double negmu = lv.negmu;
+  const int64_t okz = lv.off[nl - 1];  // level k1 = nl (k0 = 1)
+  double rz = 0.0;
+  double rho = 0.0;
+  int done = 0;
+  bool waited = false;
+  uint32_t phase = 0;
+  const int gw = blockIdx.x * WD + wid, nw = gridDim.x * WD;
+  #pragma unroll 1
+  for (int tile = gw; tile < td.ntiles; tile += nw) {
+    // ranges of the tile at every level (lane t), static segments (lane < nseg)
+    int a = 0, b = 0;
+    if (lane < nl) { a = tstart[lane * nt1 + tile]; b = tstart[lane * nt1 + tile + 1]; sa[lane] = a; sn[lane] = b - a; }
+    const int4 sd = (lane < td.nseg) ? __ldg(segs + (int64_t)tile * td.nseg + lane) : make_int4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the last tile before the copies
+    if (lane < td.nseg) {
+      const int kind = sd.x & 3, t = (sd.x >> 2) & 63, dst = sd.x >> 8;
+      if (sd.y > 0) {
+        mbar_expect_tx(bar, (uint32_t)sd.y);
+        const char* src = (kind == SEG_CP)   ? (const char*)cptr + (int64_t)sd.z * 4
+                          : (kind == SEG_KI) ? (const char*)kinv + (int64_t)sd.z * 8
+                                             : (const char*)lof + (int64_t)sd.z * 8;
+        tma_1d_keep(sm + dst, src, (uint32_t)sd.y, bar);
+      }
+      if (kind == SEG_CP) skc_[wid][t] = sd.w;
+      else if (kind == SEG_KI) skk_[wid][t] = sd.w;
+      else skl_[wid][t] = sd.w;
+    }
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+      done = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+      rho = scal[S_SHIFT];
+    }
+    const int a0 = __shfl_sync(0xffffffffu, a, 0), n0 = __shfl_sync(0xffffffffu, b - a, 0);
+    const int ak = __shfl_sync(0xffffffffu, a, m1), nk = __shfl_sync(0xffffffffu, b - a, m1);
+    if (!done) {  // dynamic segments: y_1 = r, z and w at level k1
+      if (lane == 29) skd[wid][0] = stage_window(bar, sm + td.o_y[0], rin, 8, a0, (int64_t)a0 + n0);
+      else if (lane == 30) skd[wid][1] = stage_window(bar, sm + td.o_z[m1], Zg, 8, okz + ak, okz + ak + nk);
+      else if (lane == 31) skd[wid][2] = stage_window(bar, sm + td.o_w[m1], Wg, 8, okz + ak, okz + ak + nk);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    if (done) break;  // warp-uniform; the copies have landed
+    if (lane < nl) {
+      const int t = lane;
+      LvlPtr e;
+      e.cp = (t >= 1) ? td.o_cp[t] + 4 * skc_[wid][t] : -1;
+      e.ki = (t >= 1) ? td.o_ki[t] + 8 * skk_[wid][t] : -1;
+      e.lo = (t + 1 < nl) ? td.o_lo[t] + 8 * skl_[wid][t] : -1;
+      e.y = (t == 0) ? td.o_y[0] + 8 * skd[wid][0] : (t + 1 < nl ? td.o_y[t] : -1);
+      e.nn = (t == 0) ? -1 : (t + 1 < nl ? td.o_n[t] : -1);
+      e.z = (t == m1) ? td.o_z[t] + 8 * skd[wid][1] : (t >= 1 ? td.o_z[t] : -1);
+      e.w = (t == m1) ? td.o_w[t] + 8 * skd[wid][2] : (t >= 1 ? td.o_w[t] : -1);
+      e.a = sa[t];
+      e.cnt = sn[t];
+      e.ck = lv.ck[1 + t];
+      tb[t] = e;
+    }
+    __syncwarp();
+    // ---- recompute y, N of levels 2 .. k1-1 (two levels per step where both
+    // need it: the same additions in the same order as one level at a time)
+    {
+      int t = 1;
+      #pragma unroll 1
+      for (; t + 2 < nl; t += 2) {
+        const int* cp1 = SMP(const int, tb[t].cp);
+        const int* cp2 = SMP(const int, tb[t + 1].cp);
+        const double* yg = SMP(const double, tb[t - 1].y);
+        const double* ng = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
+        double* yc = SMP(double, tb[t].y);
+        double* nc = SMP(double, tb[t].nn);
+        double* yp = SMP(double, tb[t + 1].y);
+        double* np = SMP(double, tb[t + 1].nn);
+        const int ag = tb[t - 1].a, ac = tb[t].a, npar = tb[t + 1].cnt;
+        #pragma unroll 1
+        for (int i = lane; i < npar; i += 32) {
+          const int c0 = cp2[i] - ac, c1 = cp2[i + 1] - ac;
+          double y2 = 0.0, N2 = 1.0;
+          #pragma unroll 1
+          for (int c = c0; c < c1; ++c) {
+            const int g0 = cp1[c] - ag, g1 = cp1[c + 1] - ag;
+            double y = 0.0, N = 1.0;
+            if (ng) {
+              #pragma unroll 1
+              for (int gg = g0; gg < g1; ++gg) { y += yg[gg]; N += ng[gg]; }
+            } else {
+              #pragma unroll 1
+              for (int gg = g0; gg < g1; ++gg) y += yg[gg];
+              N = (double)(1 + g1 - g0);
+            }
+            yc[c] = y;
+            nc[c] = N;
+            y2 += y;
+            N2 += N;
+          }
+          yp[i] = y2;
+          np[i] = N2;
+        }
+        __syncwarp();
+      }
+      #pragma unroll 1
+      for (; t + 1 < nl; ++t) {
+        const int* cp = SMP(const int, tb[t].cp);
+        const double* yc = SMP(const double, tb[t - 1].y);
+        const double* nc = tb[t - 1].nn >= 0 ? SMP(const double, tb[t - 1].nn) : nullptr;
+        double* yp = SMP(double, tb[t].y);
+        double* np = SMP(double, tb[t].nn);
+        const int ac = tb[t - 1].a, npar = tb[t].cnt;
+        #pragma unroll 1
+        for (int i = lane; i < npar; i += 32) {
+          const int c0 = cp[i] - ac, c1 = cp[i + 1] - ac;
+          double y = 0.0, N = 1.0;
+          if (nc) {
+            #pragma unroll 1
+            for (int c = c0; c < c1; ++c) { y += yc[c]; N += nc[c]; }
+          } else {
+            y = yc[c0] + yc[c0 + 1];
+            #pragma unroll 1
+            for (int c = c0 + 2; c < c1; ++c) y += yc[c];
+            N = (double)(1 + c1 - c0);
+          }
+          yp[i] = y;
+          np[i] = N;
+        }
+        __syncwarp();
+      }
+    }
+    // ---- down: levels k1-1 .. 2 in shared memory, then level 1 out
+    #pragma unroll 1
+    for (int t = nl - 2; t >= 1; --t) {
+      const int* cp = SMP(const int, tb[t + 1].cp);
+      const double* ki = SMP(const double, tb[t + 1].ki);
+      const double* zp = SMP(const double, tb[t + 1].z);
+      const double* wp = SMP(const double, tb[t + 1].w);
+      const double* lo = SMP(const double, tb[t].lo);
+      const double* yc = SMP(const double, tb[t].y);
+      const double* nc = SMP(const double, tb[t].nn);
+      double* zc = SMP(double, tb[t].z);
+      double* wc = SMP(double, tb[t].w);
+      const int ac = tb[t].a, npar = tb[t + 1].cnt;
+      const double ckk = tb[t].ck;
+      #pragma unroll 1
+      for (int i = lane; i < npar; i += 32) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
+            [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
+            [&](int p) { return ckk * yc[p] - rho * nc[p]; },
+            [&](int p, double z, double w) { zc[p] = z; wc[p] = w; });
+      }
+      __syncwarp();
+    }
+    {
+      const int* cp = SMP(const int, tb[1].cp);
+      const double* ki = SMP(const double, tb[1].ki);
+      const double* zp = SMP(const double, tb[1].z);
+      const double* wp = SMP(const double, tb[1].w);
+      const double* lo = SMP(const double, tb[0].lo);
+      const double* yc = SMP(const double, tb[0].y);
+      const int ac = tb[0].a, npar = tb[1].cnt;
+      double* zg = zout + (int64_t)zs * ac;
+      #pragma unroll 1
+      for (int i = lane; i < npar; i += 32) {
+        const int lb = -3 * (2 * i + 2);
+        block_solve(
+            cp[i] - ac, cp[i + 1] - ac, [&](int j) { return ki[3 * i + j]; },
+            [&](int p, int j) { return lo[lb + 3 * p + j]; }, zp[i], negmu * wp[i],
+            [&](int p) { return yc[p] - rho; },
+            [&](int p, double z, double w) { rz += yc[p] * w; zg[zs * p] = w; });
+      }
+    }
+    __syncwarp();  // every lane is done with this tile's shared memory
+  }
+  if (!waited) {  // a warp without tiles
+    pdl_wait();
+    done = (mode != M_APPLY) ? (int)cnt[C_DONE] : 0;
+  }
+  if (done) return;  // the whole grid (the flag is constant during this kernel)
+  pdl_trigger();
+  rz = block_sum<WD * 32>(rz);
+  if (threadIdx.x < 32) {  // only warp 0 waits on the ticket
+    if (threadIdx.x == 0) part[blockIdx.x] = rz;
+    if (mode != M_APPLY && warp_last_block(&cnt[C_DOWN])) {
+      const double tot = warp_sum_partials(part, gridDim.x);
+      if (threadIdx.x == 0) {
+        finish_rz(tot, scal, mode);
+        cnt[C_DOWN] = 0;
+      }
+    }
+  }
+}
+
 #undef TRACE_KID
 #define TRACE_KID 0
 // ------------------------------------------------------ per-level kernels
@@ -2102,6 +2443,35 @@ std::vector<TierRun> tier_runs(Handle& h) {
 
 enum { PH_UP_LOW = 1, PH_UPPER = 2, PH_DOWN_LOW = 4, PH_ALL = 7 };
 
+// The first tier's up sweep streamed (k_up_stream) instead of tile-staged
+// (k_tile_up<true>): measured per iteration (us) staged -> streamed, configs[2]
+// 839 -> 803, configs[3] 401 -> 392, configs[4] at scale 0.1 (a level-1-only
+// tier) 292 -> 286, but configs[1] 60.5 -> 64.2 (its 1M-row problem is small
+// enough that the staged kernel's prologue, TMA of r and H before the grid
+// dependency, overlaps a large part of the SpMV's tail).  Streamed for
+// level-1-only tiers and from 2^21 rows on; MSP_UP_STREAM=1 / 0 forces it.
+bool use_up_stream(const Handle& h, const TierRun& T) {
+  static const int v = std::getenv("MSP_UP_STREAM") ? std::atoi(std::getenv("MSP_UP_STREAM")) : -1;
+  if (v >= 0) return v != 0;
+  return T.k1 == T.k0 || h.n >= (int64_t(1) << 21);
+}
+
+// grid of k_up_stream: a few CTAs per SM (MSP_UPS_PER_SM), no more than the
+// nodes (or elements) need
+unsigned up_stream_grid(const Handle& h, const TierRun& T) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    MSP_CUDA(cudaGetDevice(&dev));
+    MSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  int per_sm = 4;
+  if (const char* e = std::getenv("MSP_UPS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+  const int64_t need = (T.k1 == T.k0) ? (h.n + UT * 4 - 1) / (UT * 4)
+                                      : (h.lv[T.k1 - 1].n + UT / MSP_FLAT_G - 1) / (UT / MSP_FLAT_G);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
+}
+
 // R r (MSP) on nested vectors.  mode APPLY: r -> z;  INIT / ITER: the PCG
 // step (ITER first updates r) with the scalars of reading R10.  Tiers
 // 0..tp are the "low" ones (a rank's own part when distributed: M_DIST makes
@@ -2117,12 +2487,25 @@ void msp_sweeps_runs(Handle& h, const Lv& lv, const std::vector<TierRun>& runs, 
   double* scal = h.scal.p;
   const int nt = (int)runs.size();
   const bool dist = (mode & M_DIST) != 0;
-  const int npart_up = runs.empty() || runs[0].generic ? 0 : (int)((runs[0].ntiles + runs[0].up_group - 1) / runs[0].up_group);
+  // the first tier's up sweep streamed (k_up_stream) on one GPU
+  const bool stream = !dist && !runs.empty() && !runs[0].generic && runs[0].k0 == 1 && use_up_stream(h, runs[0]);
+  const unsigned sgrid = stream ? up_stream_grid(h, runs[0]) : 0u;
+  const int npart_up = runs.empty() || runs[0].generic
+                           ? 0
+                           : stream ? (int)sgrid : (int)((runs[0].ntiles + runs[0].up_group - 1) / runs[0].up_group);
   auto up = [&](int i) {
     const TierRun& T = runs[i];
     const int md = (i <= tp) ? mode : (mode & ~M_DIST);
     P.begin();
-    if (T.generic) {
+    if (i == 0 && stream) {
+      if (T.k1 == T.k0)
+        launch_c(4, k_up_stream<true>, sgrid, UT, 0, st, (int64_t)0, (const int32_t*)nullptr, h.n, q, r,
+                 (const double*)h.Hvec.p, (double*)nullptr, part_rr, part_gd, scal, cnt, md);
+      else
+        launch_c(4, k_up_stream<false>, sgrid, UT, 0, st, h.lv[T.k1 - 1].n, T.firstk0, h.n, q, r,
+                 (const double*)h.Hvec.p, h.Y.p + h.lv[T.k1 - 1].off, part_rr, part_gd, scal, cnt, md);
+      P.end(PC_TILE_UP);
+    } else if (T.generic) {
       const int k = T.k0;
       const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
       launch_c(16, k_up_lvl, grid_for(std::max<int64_t>(T.nB, 1)) + T.nheavy, TPB, 0, st, lv, k,
@@ -2163,7 +2546,11 @@ void msp_sweeps_runs(Handle& h, const Lv& lv, const std::vector<TierRun>& runs, 
                  cnt, md & ~M_DIST, T.heavy, T.nheavy, T.B0, T.nB);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
-      if (T.k0 == 1)
+      if (T.k0 == 1 && !dist && h.wdown_grid > 0)
+        launch_c(8, k_wtile_down, h.wdown_grid, WD * 32, (size_t)WD * h.wdown_region, st, lv, *T.desc, T.tstart,
+                 (const int32_t*)h.cptr.p, (const double*)h.kinv.p, (const double*)h.lof.p, (const double*)r,
+                 (const double*)h.Z.p, (const double*)h.W.p, z, part_rz, scal, cnt, md, T.segs, h.wdown_region);
+      else if (T.k0 == 1)
         launch_c(8, k_tile_down<true>, (unsigned)std::max<int64_t>(1, (T.ntiles + T.tpc - 1) / T.tpc), TT,
                  T.smem_down, st, lv, *T.desc, T.tstart, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                  (const double*)h.lof.p, (const double*)h.Nsub.p, (const double*)r, h.Z.p, h.W.p, z, part_rz, scal,
@@ -2230,7 +2617,8 @@ void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q
     launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
            (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(), (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
-           reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1);
+           reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1,
+           (const double*)nullptr, (const double*)nullptr, (double*)nullptr);
   };
   if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true>);
@@ -2241,9 +2629,44 @@ void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q
   ++h.launches;
 }
 
+// SpMV of the MSP iteration on separate z, p_old, p vectors (the pipelined
+// kernel, full-sector stores)
+void launch_spmv_sep(Handle& h, const double* z, const double* pold, double* pnew, double* q, double* x,
+                     cudaStream_t st, int64_t row0 = 0, int64_t row1 = -1) {
+  if (row1 < 0) row1 = h.n;
+  auto go = [&](auto kern) {
+    launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
+             (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
+             (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
+             (const double2*)nullptr, (double*)nullptr, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1, z, pold,
+             pnew);
+  };
+  if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true, true>);
+  else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true, true>);
+  else if (h.sell_uniform && h.sell_maxw == 8) go(k_spmv_pipe<8, true, true>);
+  else if (h.sell_maxw <= 4) go(k_spmv_pipe<4, false, true>);
+  else if (h.sell_maxw <= 8) go(k_spmv_pipe<8, false, true>);
+  else go(k_spmv_pipe<16, false, true>);
+  ++h.launches;
+}
+
+// Separate vectors unless the graph has long (power-law hub) rows: a gather
+// of (z_j, p_j) is then one sector instead of two, which wins on scattered
+// neighbours (configs[4] at scale 0.1: 292 vs 304 us per iteration), while
+// on meshes the pair layout's half-sector stores cost an L2 fill each
+// (configs[2]: 941 -> 840, configs[1]: 61.4 -> 60.5 us per iteration with
+// separate vectors).  MSP_SPMV_SEP=1 / 0 forces either.
+bool use_sep(const Handle& h) {
+  static const int mode = std::getenv("MSP_SPMV_SEP") ? std::atoi(std::getenv("MSP_SPMV_SEP")) : -1;
+  static const bool off = std::getenv("MSP_NO_SPMV_PIPE") != nullptr;
+  if (off || h.sell_maxw > 16) return false;
+  if (mode >= 0) return mode == 1;
+  return h.nlong == 0 && h.nhuge == 0;
+}
+
 bool use_pairs(const Handle& h) {
   static const bool off = std::getenv("MSP_NO_SPMV_PIPE") != nullptr;
-  return !off && h.sell_maxw <= 16;
+  return !off && h.sell_maxw <= 16 && !use_sep(h);
 }
 
 // one PCG iteration (reading R10): p = z + beta p, q = L p (x += alpha p
@@ -2264,7 +2687,8 @@ void pcg_iteration(Handle& h, const Lv& lv, int precond, double* x, cudaStream_t
   h.pparity ^= 1;
   const double* z = (precond == MSP_PRECOND_MSP) ? h.vz.p : h.vr.p;
   P.begin();
-  launch_spmv<true>(h, z, pold, pnew, h.vq.p, x, st);
+  if (precond == MSP_PRECOND_MSP && use_sep(h)) launch_spmv_sep(h, z, pold, pnew, h.vq.p, x, st);
+  else launch_spmv<true>(h, z, pold, pnew, h.vq.p, x, st);
   P.end(PC_SPMV);
   if (precond == MSP_PRECOND_MSP) {
     msp_sweeps(h, lv, h.vq.p, h.vr.p, h.vz.p, st, M_ITER, P);
@@ -2378,7 +2802,7 @@ void alloc_solve_workspace(Handle& h) {
     MSP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     // pipelined SpMV: 4 CTAs/SM (its register budget); the plain one: 8
     // (configs[3]: 426 -> 397 us/iteration)
-    int per_sm = use_pairs(h) ? 4 : 8;
+    int per_sm = (use_pairs(h) || use_sep(h)) ? 4 : 8;
     if (const char* e = std::getenv("MSP_SPMV_BLOCKS_PER_SM")) per_sm = std::max(1, std::atoi(e));
     const int64_t want = grid_for(std::max<int64_t>(h.nslices, 1) * 32);
     h.spmv_grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * per_sm);
@@ -2427,6 +2851,24 @@ void alloc_solve_workspace(Handle& h) {
   for (auto f : {(const void*)k_tile_up<true>, (const void*)k_tile_up<false>, (const void*)k_tile_down<true>,
                  (const void*)k_tile_down<false>})
     MSP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  // warp-per-tile first-tier down kernel: WD regions per CTA, about one
+  // wave of resident CTAs (each warp then strides over the tiles)
+  h.wdown_grid = 0;
+  if (h.wdown && !h.tiers.empty() && !h.tiers[0].generic && h.tiers[0].k0 == 1 && h.tiers[0].k1 > 1) {
+    auto& T = h.tiers[0];
+    h.wdown_region = (int)((T.smem_down + 127) & ~(size_t)127);
+    const size_t smem = (size_t)WD * h.wdown_region;
+    if (smem <= 220 * 1024) {
+      raise_smem_limit((const void*)k_wtile_down, smem);
+      MSP_CUDA(cudaFuncSetAttribute((const void*)k_wtile_down, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      int per_sm = 0, dev = 0, nsm = 0;
+      MSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_wtile_down, WD * 32, smem));
+      MSP_CUDA(cudaGetDevice(&dev));
+      MSP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      const int64_t want = (T.ntiles + WD - 1) / WD;
+      h.wdown_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::max(per_sm, 1) * nsm));
+    }
+  }
   raise_smem_limit((const void*)k_coarse, h.coarse_smem);
   // merged last-tier down + coarse kernel (tier k1 == Kc, small top)
   h.merged_coff = 0;

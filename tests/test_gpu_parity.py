@@ -348,6 +348,38 @@ def test_full_size_config1_apply_R_and_pcg():
     assert np.linalg.norm(r - L @ x) <= 2e-8 * np.linalg.norm(r)
 
 
+FULL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full_size")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(FULL, "cfg1_pcg_msp.npz")),
+                    reason="oracle record not generated (tools/oracle_record.py --config 1)")
+def test_full_size_config1_pcg_against_oracle_record():
+    """configs[1] at full size (1,048,576 vertices): the GPU PCG-MSP solve
+    against the oracle's own full-size solve, recorded by
+    tools/oracle_record.py (oracle/ and inputs/ only; the same b, hierarchy
+    seed and mu).  Iterations within R11's band: +-2, or the spread of the
+    oracle's own count under a 1e-15 relative perturbation of b (the _p1
+    record); solution within 1e-8 relative in the L-norm."""
+    rec = np.load(os.path.join(FULL, "cfg1_pcg_msp.npz"))
+    g = G.config_graph(1)
+    s = gpu_setup(g, float(rec["mu"]), 0, int(rec["hierarchy_seed"]))
+    b = G.rhs(g.n, int(rec["rhs_seed"]))
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=100000)
+    assert out["converged"] == 1 and bool(rec["converged"])
+    band = 2
+    pp = os.path.join(FULL, "cfg1_pcg_msp_p1.npz")
+    if os.path.exists(pp):
+        band = max(2, abs(int(np.load(pp)["iterations"]) - int(rec["iterations"])))
+    record("config1_full_pcg", "iterations", abs(out["iterations"] - int(rec["iterations"])), band)
+    L = GR.laplacian_of_graph(g)
+    x = out["x"].cpu().numpy()
+    xr = rec["x"]
+    e = x - xr
+    e -= e.mean()
+    xs = xr - xr.mean()
+    record("config1_full_pcg", "x_Lnorm", float(np.sqrt(abs(e @ (L @ e))) / np.sqrt(xs @ (L @ xs))), 1e-8)
+
+
 @pytest.mark.parametrize("tpc", [2, 3, 7])
 def test_multi_tile_down_ctas(tpc):
     """Several first-tier tiles per CTA of the down kernel (MSP_DOWN_TPC;

@@ -6,7 +6,7 @@ cfg=${1:-2}; tag=${2:-p}; it=${3:-12}
 mkdir -p gpurun_out
 export MSP_NO_GRAPH=1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none \
-   -k "regex:^k_(spmv|tile_up|tile_down|coarse|up_lvl|down_lvl|x_final|init_state|gather|scatter)" -c 400 --csv \
+   -k "regex:^k_(spmv|tile_up|tile_down|up_stream|wtile_down|coarse|up_lvl|down_lvl|x_final|init_state|gather|scatter)" -c 400 --csv \
    --log-file gpurun_out/${tag}_launches_cfg${cfg}.csv python tools/ncu_driver.py --config $cfg --iters $it \
    > gpurun_out/${tag}_launch.log 2>&1
 for k in "k_tile_down<.bool.1, .bool.0>" ; do
