@@ -113,6 +113,18 @@ struct Handle {
   // per-level sweep kernels
   DBuf<int32_t> heavy;
   std::vector<int64_t> heavy_off;
+  // their chunks (sched.cuh HeavyChunks), per parent level k+1: chunks
+  // hch_off[k-1] .. hch_off[k)
+  DBuf<int4> hch_seg;
+  std::vector<int64_t> hch_off;
+  DBuf<int32_t> hch_first;
+  DBuf<unsigned> hch_cnt;
+  DBuf<double> hch_part, hch_sum, hch_cst;
+  HeavyChunks heavy_chunks(int k) const {  // parent level k+1
+    if (hch_off.empty() || hch_off[k] == hch_off[k - 1]) return HeavyChunks{nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+    return HeavyChunks{hch_seg.p + hch_off[k - 1], (int)(hch_off[k] - hch_off[k - 1]), hch_first.p, hch_cnt.p,
+                       hch_part.p, hch_sum.p, hch_cst.p, (int)hch_off[k - 1]};
+  }
   // MSP block-tree factors, packed:
   //   kinv[3 (off_{k+1} - n + B) + {0,1,2}] = K'^{-1} (uu, uv, vv) of aggregate B at level k+1
   //   lof[3 (lo_off[k-1] + p - 2B - 2) + {0,1,2}] = (s w_xu / d, s w_xv / d, 1 / d) of leftover p
@@ -129,7 +141,7 @@ struct Handle {
   // ---- level-1 Laplacian in SELL-32 (slices of 32 rows, column-major,
   // padded with (self, 0)); rows of degree > LCAP are "long": empty in SELL,
   // flagged in sell_mask and handled warp-per-row from the nested CSR
-  int64_t nslices = 0, nlong = 0, nhuge = 0;  // long rows: warp per row; huge: CTA per row (after them)
+  int64_t nslices = 0, nlong = 0, nhuge = 0, nmed = 0;  // long_rows: [0, nmed) medium, [nmed, nlong) long, then huge  // long rows: warp per row; huge: CTA per row (after them)
   int sell_maxw = 0;          // widest slice (padded row length)
   bool sell_uniform = false;  // every slice padded to sell_maxw (no slice pointers needed)
   DBuf<int64_t> sell_ptr;
@@ -244,6 +256,7 @@ void dist_range(const Handle& h, int64_t* out8);
 void add_into(Handle& h, const double* a, double* y, cudaStream_t st);
 void alloc_solve_workspace(Handle& h);
 void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
+void build_heavy_chunks(Handle& h, cudaStream_t st);  // setup.cu: chunks of the heavy aggregates
 // pegp.cu
 void pegp_build(Handle& h, cudaStream_t st);
 void apply_LH_nested(Handle& h, const double* x, double* y, cudaStream_t st);

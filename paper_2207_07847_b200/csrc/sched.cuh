@@ -21,6 +21,7 @@ constexpr int MAXL = 40;   // levels
 // the CTA that finishes a row's last segment (ticket cnt[row]) sums the
 // row's partials in segment order (deterministic) and writes the row.
 constexpr int HUGE_SEG = 16384;
+constexpr int MED_ROW = 64;  // medium rows (lcap < degree <= MED_ROW): 8 lanes per row in the SpMV
 struct HugeDesc {
   const int4* seg;       // [nseg]: x = huge-row index (into long_rows[nlong + x]), y = e0, z = e1
   int64_t nseg;
@@ -29,6 +30,26 @@ struct HugeDesc {
   double* part;          // [nseg]: segment partial sums
 };
 constexpr int MAXT = 16;   // levels per tier
+
+// Heavy aggregates (more than HEAVY_AGG children; power-law hubs hold up to
+// millions) of one parent level, cut into chunks of at most HEAVY_CHUNK
+// children, a CTA each in the generic per-level sweeps.  The up kernel sums
+// y and the leftover-weighted sums S_j = sum_x C(x, j) y_x (j = 0, 1) per
+// chunk; the CTA that finishes an aggregate's last chunk (ticket cnt[h])
+// adds the chunk partials in chunk order (deterministic).  The down kernel's
+// chunks then need no reduction: sum_x C(x, j) t_x = c(k) S_j - rho K_j with
+// K_j = sum_x C(x, j) N_x fixed at setup.
+constexpr int HEAVY_CHUNK = 4096;
+struct HeavyChunks {
+  const int4* seg;      // [nch]: x = aggregate B (nested, parent level), y = first child, z = end, w = heavy index h
+  int nch;              // chunks of this level (0: CTA-per-aggregate path)
+  const int32_t* first; // [nheavy_total + 1]: first chunk (global) of heavy aggregate h
+  unsigned* cnt;        // [nheavy_total]: tickets (zero between launches)
+  double* part;         // [3 * chunks_total]: per-chunk (sum y, S_0, S_1)
+  double* sum;          // [2 * nheavy_total]: (S_0, S_1) of the last up sweep
+  const double* cst;    // [2 * nheavy_total]: (K_0, K_1)
+  int c0;               // global index of this level's first chunk
+};
 
 struct Lv {
   int L, Kc;

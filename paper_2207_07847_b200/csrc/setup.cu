@@ -452,7 +452,9 @@ __global__ void k_sell_width(int64_t n, int64_t nslices, const int32_t* __restri
   int deg = 0;
   if (r < n) deg = rowptr[r + 1] - rowptr[r];
   const bool lng = deg > lcap;
-  if (r < n) islong[r] = lng ? (deg > hcap ? 2 : 1) : 0;
+  // 1: medium (lcap < deg <= MED_ROW: 8 lanes per row), 3: long (a warp),
+  // 2: huge (CTA segments)
+  if (r < n) islong[r] = lng ? (deg > hcap ? 2 : (deg > MED_ROW ? 3 : 1)) : 0;
   int w = lng ? 0 : deg;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
@@ -954,6 +956,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     GN += reduce_sum(tmp, gpart.p, nk1, st);
   }
   h.GN = GN;
+  build_heavy_chunks(h, st);
   clk.mark(st, "factors");
 
   // ---- gdot weights H = G_1 (top-down over the hierarchy)
@@ -978,9 +981,11 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
   clk.mark(st, "gdot weights");
   // ---- level-1 Laplacian in SELL-32 for the solve
   {
-    // rows above lcap go to the warp-per-row path: 64 by default; 16 for a
-    // heavy-tailed degree distribution (max degree > 64 x mean), whose few
-    // long rows would otherwise pad most slices
+    // rows above lcap leave the SELL slices: 64 by default; 8 for a
+    // heavy-tailed degree distribution (max degree > 64 x mean), whose
+    // nested order mixes row lengths within a slice (SELL padding at
+    // configs[4] scale 0.1: 2.6x of the entries at lcap 8, 3.0x at 16, 4.8x
+    // at 64); rows of lcap+1 .. MED_ROW entries take 8 lanes each
     int lcap = 64;
     {
       DBuf<int> md;
@@ -989,7 +994,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
       k_max_degree<<<grid_for(n), TPB, 0, st>>>(n, h.rowptr1.p, md.p);
       MSP_LAUNCH_CHECK();
       const int maxdeg = d2h_scalar(md.p, st);
-      if ((double)maxdeg > 64.0 * (double)h.nnz_adj / (double)n) lcap = 16;
+      if ((double)maxdeg > 64.0 * (double)h.nnz_adj / (double)n) lcap = 8;
     }
     if (const char* e = std::getenv("MSP_SELL_LCAP")) lcap = std::max(1, std::atoi(e));
     const int64_t ns = (n + 31) / 32;
@@ -1026,7 +1031,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     k_sell_fill<<<grid_for(ns * 32), TPB, 0, st>>>(n, ns, h.sell_ptr.p, h.rowptr1.p, h.col1.p, h.w1.p,
                                                    h.sell_mask.p, h.sell_col.p, h.sell_w.p);
     MSP_LAUNCH_CHECK();
-    // long rows, in increasing order (deterministic)
+    // medium, long and huge rows, each class in increasing order (deterministic)
     DBuf<int32_t> ids, nsel;
     ids.alloc(n);
     nsel.alloc(1);
@@ -1036,9 +1041,14 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     fl.alloc(n);
     size_t bytes = 0;
     MSP_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids.p, fl.p, h.long_rows.p, nsel.p, n, st));
+    // medium rows first, then the long ones (both "long" for the SpMV
+    // kernels that take a warp per row: nlong counts both)
     k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 1, fl.p);
     MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p, nsel.p, n, st));
-    h.nlong = d2h_scalar(nsel.p, st);
+    h.nmed = d2h_scalar(nsel.p, st);
+    k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 3, fl.p);
+    MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p + h.nmed, nsel.p, n, st));
+    h.nlong = h.nmed + d2h_scalar(nsel.p, st);
     k_flag_eq<<<grid_for(n), TPB, 0, st>>>(n, islong.p, 2, fl.p);  // huge rows follow the long ones
     MSP_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes), bytes, ids.p, fl.p, h.long_rows.p + h.nlong, nsel.p, n, st));
     h.nhuge = d2h_scalar(nsel.p, st);
@@ -1250,6 +1260,84 @@ std::vector<int4> make_tile_segs(const Handle& h, int k0_, int nl, const TierDes
     }
   }
   return segs;
+}
+
+// K_j = sum over the leftovers x of heavy aggregate h of C(x, j) N_x (one
+// CTA per heavy aggregate, fixed-order block sum; setup only)
+__global__ void k_heavy_const(int64_t nh, const int32_t* __restrict__ heavy, const int32_t* __restrict__ cp,
+                              const double* __restrict__ lof, const double* __restrict__ Nk, int64_t lo_k,
+                              double* __restrict__ cst) {
+  const int64_t B = heavy[blockIdx.x];
+  const int64_t s0 = cp[B], s1 = cp[B + 1];
+  const int64_t lb = 3 * (lo_k - 2 * B - 2);
+  double a = 0.0, b = 0.0;
+  for (int64_t p = s0 + 2 + threadIdx.x; p < s1; p += blockDim.x) {
+    a += lof[lb + 3 * p + 0] * Nk[p];
+    b += lof[lb + 3 * p + 1] * Nk[p];
+  }
+  __shared__ double sa[256], sb[256];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) { ta += sa[i]; tb += sb[i]; }
+    cst[2 * blockIdx.x] = ta;
+    cst[2 * blockIdx.x + 1] = tb;
+  }
+}
+
+// Chunks of the heavy aggregates (sched.cuh HeavyChunks)
+void build_heavy_chunks(Handle& h, cudaStream_t st) {
+  const int L = h.levels;
+  h.hch_off.assign(L, 0);
+  const int64_t nh = h.heavy_off.empty() ? 0 : h.heavy_off[L - 1];
+  if (nh == 0) { h.hch_off.clear(); return; }
+  int64_t CH = HEAVY_CHUNK;  // MSP_HEAVY_CHUNK: smaller chunks for tests of the multi-chunk path
+  if (const char* e = std::getenv("MSP_HEAVY_CHUNK")) CH = std::max<int64_t>(2, std::atoll(e));
+  std::vector<int4> segs;
+  std::vector<int32_t> first(nh + 1, 0);
+  for (int k = 1; k < L; ++k) {
+    h.hch_off[k - 1] = (int64_t)segs.size();
+    const int64_t a = h.heavy_off[k - 1], b = h.heavy_off[k];
+    if (b == a) continue;
+    std::vector<int32_t> ids(b - a);
+    MSP_CUDA(cudaMemcpyAsync(ids.data(), h.heavy.p + a, (b - a) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    const int64_t nB = h.lv[k].n;
+    std::vector<int32_t> cp(nB + 1);
+    MSP_CUDA(cudaMemcpyAsync(cp.data(), h.cptr.p + h.cptr_off[k - 1], (nB + 1) * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, st));
+    MSP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < b - a; ++i) {
+      const int32_t B = ids[i];
+      first[a + i] = (int32_t)segs.size();
+      for (int64_t c = cp[B]; c < cp[B + 1]; c += CH)
+        segs.push_back(make_int4(B, (int)c, (int)std::min<int64_t>(c + CH, cp[B + 1]), (int)(a + i)));
+    }
+    h.hch_off[k] = (int64_t)segs.size();
+  }
+  h.hch_off[L - 1] = (int64_t)segs.size();
+  for (int k = 1; k < L; ++k) h.hch_off[k] = std::max(h.hch_off[k], h.hch_off[k - 1]);
+  first[nh] = (int32_t)segs.size();
+  h.hch_seg.alloc(segs.size());
+  MSP_CUDA(cudaMemcpyAsync(h.hch_seg.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+  h.hch_first.alloc(nh + 1);
+  MSP_CUDA(cudaMemcpyAsync(h.hch_first.p, first.data(), (nh + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  h.hch_cnt.alloc(nh);
+  MSP_CUDA(cudaMemsetAsync(h.hch_cnt.p, 0, nh * sizeof(unsigned), st));
+  h.hch_part.alloc(3 * segs.size());
+  h.hch_sum.alloc(2 * nh);
+  MSP_CUDA(cudaMemsetAsync(h.hch_sum.p, 0, 2 * nh * sizeof(double), st));
+  h.hch_cst.alloc(2 * nh);
+  for (int k = 1; k < L; ++k) {
+    const int64_t a = h.heavy_off[k - 1], b = h.heavy_off[k];
+    if (b == a) continue;
+    k_heavy_const<<<(unsigned)(b - a), 256, 0, st>>>(b - a, h.heavy.p + a, h.cptr.p + h.cptr_off[k - 1], h.lof.p,
+                                                     h.Nsub.p + h.lv[k - 1].off, h.lo_off[k - 1],
+                                                     h.hch_cst.p + 2 * a);
+  }
+  MSP_LAUNCH_CHECK();
+  MSP_CUDA(cudaStreamSynchronize(st));
 }
 
 // Tiers and tiles of the solve schedule.

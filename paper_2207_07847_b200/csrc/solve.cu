@@ -338,7 +338,9 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
 
 // sum_e w_e (pi - p(col_e)) over e = e0 + sub, e0 + sub + S, ... < e1 with
 // four independent chains (the column and gather loads of four entries are
-// in flight together: long rows are latency bound otherwise)
+// in flight together: long rows are latency bound otherwise).  (A
+// predicated last group instead of the scalar tail measured no faster on
+// configs[4].)
 template <int S, typename PJ>
 __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col, const double* __restrict__ w, int32_t e0,
                                           int32_t e1, int sub, double pi, PJ pj) {
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
                                                       double* __restrict__ part, double* __restrict__ scal,
                                                       unsigned int* __restrict__ cnt, int64_t row0, int64_t row1,
                                                       const double* __restrict__ zs, const double* __restrict__ ps,
-                                                      double* __restrict__ pn) {
+                                                      double* __restrict__ pn, int64_t nmed) {
   // pairs (!SEP): zp[i] = (z_i, p_old_i), the new p_i goes to zpout[2 i + 1];
   // SEP: z, p_old and the new p in three plain vectors zs, ps, pn (every
   // store a full sector: no L2 fill of a half-written pair line).  Rows
@@ -645,12 +647,42 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     b1 = n1;
     if (s < s_end) load_B(s, b0, b1);
   }
-  for (int64_t i = warp; i < nlong; i += nwarps) {  // warp per long row
+  {  // medium rows: 8 lanes per row, four rows per warp (warp-uniform trip count)
+    constexpr int MG = 8;
+    const int sub = lane & (MG - 1);
+    for (int64_t base = warp * (32 / MG); base < nmed; base += nwarps * (32 / MG)) {
+      const int64_t i = base + lane / MG;
+      const bool ok = i < nmed;
+      const int64_t r = ok ? long_rows[i] : 0;
+      const bool mine = ok && r >= row0 && r < row1;
+      double pi = 0.0, pr = 0.0, xr = 0.0, acc = 0.0;
+      if (mine) {
+        const double2 vr = zpj(r);
+        pr = vr.y;
+        pi = vr.x + beta * pr;
+        if (sub == 0) xr = x[r];
+        acc = row_dot<MG>(col, w, rowptr[r], rowptr[r + 1], sub, pi, [&](int32_t j) {
+          const double2 v = zpj(j);
+          return v.x + beta * v.y;
+        });
+      }
+#pragma unroll
+      for (int o = MG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (mine && sub == 0) {
+        q[r] = acc;
+        put_p(r, pi);
+        x[r] = xr + alpha * pr;
+        d += pi * acc;
+      }
+    }
+  }
+  for (int64_t i = nmed + warp; i < nlong; i += nwarps) {  // warp per long row
     const int64_t r = long_rows[i];
     if (r < row0 || r >= row1) continue;
     const double2 vr = zpj(r);
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
+    const double xr = (lane == 0) ? x[r] : 0.0;  // in flight with the row
     double acc = row_dot<32>(col, w, rowptr[r], rowptr[r + 1], lane, pi, [&](int32_t j) {
       const double2 v = zpj(j);
       return v.x + beta * v.y;
@@ -659,7 +691,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     if (lane == 0) {
       q[r] = acc;
       put_p(r, pi);
-      x[r] += alpha * pr;
+      x[r] = xr + alpha * pr;
       d += pi * acc;
     }
   }
@@ -1947,15 +1979,55 @@ __global__ void __launch_bounds__(WD * 32) k_wtile_down(const __grid_constant__ 
 __global__ void __launch_bounds__(TPB) k_up_lvl(const __grid_constant__ Lv lv, int k, const int32_t* __restrict__ cptr,
                                                 const double* __restrict__ yin, double* __restrict__ yout,
                                                 const unsigned int* __restrict__ cnt, int mode_in,
-                                                const int32_t* __restrict__ heavy, int nheavy, int64_t B0, int64_t nB) {
+                                                const int32_t* __restrict__ heavy, int nheavy, int64_t B0, int64_t nB,
+                                                const HeavyChunks hc, const double* __restrict__ lof) {
   // parents B0 .. B0+nB-1 of level k+1 (a rank's own range; all of them on one GPU)
-  // blocks [0, G - nheavy): a thread per aggregate (heavy ones skipped);
-  // blocks [G - nheavy, G): a CTA per heavy aggregate
+  // blocks [0, G - nheavy - nch): a thread per aggregate (heavy ones skipped);
+  // then a CTA per heavy aggregate (nheavy) or per heavy chunk (hc.nch)
   const int mode = mode_in & 15;
   pdl_wait();
   if (mode == M_ITER && cnt[C_DONE]) return;
   const int32_t* cp = cptr + lv.cpo[k - 1];
-  const int nnorm = (int)gridDim.x - nheavy;
+  if ((int)blockIdx.x >= (int)gridDim.x - hc.nch) {  // a chunk of a heavy aggregate
+    const int c = (int)blockIdx.x - ((int)gridDim.x - hc.nch);
+    const int4 sg = hc.seg[c];
+    const int64_t B = sg.x, s0 = cp[B];
+    const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
+    double y = 0.0, a = 0.0, b = 0.0;
+    for (int64_t p = sg.y + threadIdx.x; p < sg.z; p += TPB) {
+      const double v = yin[p];
+      y += v;
+      if (p >= s0 + 2) {
+        a += lof[lb + 3 * p + 0] * v;
+        b += lof[lb + 3 * p + 1] * v;
+      }
+    }
+    const double2 yb = block_sum2<TPB>(make_double2(y, a));
+    const double bb = block_sum<TPB>(b);
+    if (threadIdx.x == 0) {
+      const int g = hc.c0 + c;
+      hc.part[3 * g] = yb.x;
+      hc.part[3 * g + 1] = yb.y;
+      hc.part[3 * g + 2] = bb;
+      __threadfence();
+      const int f0 = hc.first[sg.w], f1 = hc.first[sg.w + 1];
+      if (atomicAdd(&hc.cnt[sg.w], 1u) == (unsigned)(f1 - f0 - 1)) {  // the aggregate's last chunk
+        __threadfence();
+        double ty = 0.0, ta = 0.0, tb = 0.0;
+        for (int j = f0; j < f1; ++j) {
+          ty += __ldcg(hc.part + 3 * j);
+          ta += __ldcg(hc.part + 3 * j + 1);
+          tb += __ldcg(hc.part + 3 * j + 2);
+        }
+        yout[B] = ty;
+        hc.sum[2 * sg.w] = ta;
+        hc.sum[2 * sg.w + 1] = tb;
+        hc.cnt[sg.w] = 0;
+      }
+    }
+    return;
+  }
+  const int nnorm = (int)gridDim.x - nheavy - hc.nch;
   if ((int)blockIdx.x < nnorm) {
     const int64_t B = B0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (B < B0 + nB) {
@@ -1986,7 +2058,7 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
                                                   double* __restrict__ part, double* __restrict__ scal,
                                                   unsigned int* __restrict__ cnt, int mode_in,
                                                   const int32_t* __restrict__ heavy, int nheavy, int64_t B0,
-                                                  int64_t nB) {
+                                                  int64_t nB, const HeavyChunks hc) {
   const int mode = mode_in & 15;
   const bool dist = (mode_in & M_DIST) != 0;
   const int zs = (mode_in & M_ZS2) ? 2 : 1;
@@ -2002,8 +2074,28 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
     if (LEVEL1) { rz += yk[p] * w; wk[zs * p] = w; }
     else { zk[p] = z; wk[p] = w; }
   };
-  const int nnorm = (int)gridDim.x - nheavy;
-  if ((int)blockIdx.x < nnorm) {
+  const int nnorm = (int)gridDim.x - nheavy - hc.nch;
+  if ((int)blockIdx.x >= nnorm + nheavy) {  // a chunk of a heavy aggregate: no reduction needed
+    const int4 sg = hc.seg[(int)blockIdx.x - nnorm - nheavy];
+    const int64_t B = sg.x, s0 = cp[B];
+    const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
+    const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
+    const double kuu = ki[0], kuv = ki[1], kvv = ki[2];
+    const double zb = zB[B], wbm = lv.negmu * wB[B];
+    // sum_x C(x, j) t_x = c(k) S_j - rho K_j (t_x = c(k) y_x - rho N_x)
+    const double au = tf(s0) + (ckk * hc.sum[2 * sg.w] - rho * hc.cst[2 * sg.w]);
+    const double av = tf(s0 + 1) + (ckk * hc.sum[2 * sg.w + 1] - rho * hc.cst[2 * sg.w + 1]);
+    const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
+    if (threadIdx.x == 0 && sg.y == s0) {
+      { const double z = zb + zu; ef(s0, z, z + wbm); }
+      { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
+    }
+    for (int64_t p = max((int64_t)sg.y, s0 + 2) + threadIdx.x; p < sg.z; p += TPB) {
+      const double zx = lof[lb + 3 * p + 2] * tf(p) + lof[lb + 3 * p + 0] * zu + lof[lb + 3 * p + 1] * zv;
+      const double z = zb + zx;
+      ef(p, z, z + wbm);
+    }
+  } else if ((int)blockIdx.x < nnorm) {
     const int64_t B = B0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (B < B0 + nB && cp[B + 1] - cp[B] <= HEAVY_AGG) {
       const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
@@ -2508,9 +2600,11 @@ void msp_sweeps_runs(Handle& h, const Lv& lv, const std::vector<TierRun>& runs, 
     } else if (T.generic) {
       const int k = T.k0;
       const double* yin = (k == 1) ? r : h.Y.p + h.lv[k - 1].off;
-      launch_c(16, k_up_lvl, grid_for(std::max<int64_t>(T.nB, 1)) + T.nheavy, TPB, 0, st, lv, k,
-               (const int32_t*)h.cptr.p, yin, h.Y.p + h.lv[k].off, (const unsigned*)cnt, md, T.heavy, T.nheavy, T.B0,
-               T.nB);
+      const HeavyChunks hc = dist ? HeavyChunks{} : h.heavy_chunks(k);
+      const int nhv = hc.nch > 0 ? 0 : T.nheavy;
+      launch_c(16, k_up_lvl, grid_for(std::max<int64_t>(T.nB, 1)) + nhv + hc.nch, TPB, 0, st, lv, k,
+               (const int32_t*)h.cptr.p, yin, h.Y.p + h.lv[k].off, (const unsigned*)cnt, md, T.heavy, nhv, T.B0,
+               T.nB, hc, (const double*)h.lof.p);
       P.end(PC_MID_UP);
     } else {
       const unsigned grid = (unsigned)std::max<int64_t>(1, (T.ntiles + T.up_group - 1) / T.up_group);
@@ -2533,17 +2627,19 @@ void msp_sweeps_runs(Handle& h, const Lv& lv, const std::vector<TierRun>& runs, 
     if (T.generic) {
       const int k = T.k0;
       const int64_t ok = h.lv[k - 1].off, op = h.lv[k].off;
-      const unsigned grid = grid_for(std::max<int64_t>(T.nB, 1)) + T.nheavy;
+      const HeavyChunks hc = dist ? HeavyChunks{} : h.heavy_chunks(k);
+      const int nhv = hc.nch > 0 ? 0 : T.nheavy;
+      const unsigned grid = grid_for(std::max<int64_t>(T.nB, 1)) + nhv + hc.nch;
       if (k == 1)
         launch_c(16, k_down_lvl<true>, grid, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                  (const double*)h.lof.p, (const double*)r, (const double*)h.Nsub.p, (const double*)(h.Z.p + op),
-                 (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt, md, T.heavy, T.nheavy, T.B0,
-                 T.nB);
+                 (const double*)(h.W.p + op), (double*)nullptr, z, part_rz, scal, cnt, md, T.heavy, nhv, T.B0,
+                 T.nB, hc);
       else
         launch_c(16, k_down_lvl<false>, grid, TPB, 0, st, lv, k, (const int32_t*)h.cptr.p, (const double*)h.kinv.p,
                  (const double*)h.lof.p, (const double*)(h.Y.p + ok), (const double*)h.Nsub.p,
                  (const double*)(h.Z.p + op), (const double*)(h.W.p + op), h.Z.p + ok, h.W.p + ok, part_rz, scal,
-                 cnt, md & ~M_DIST, T.heavy, T.nheavy, T.B0, T.nB);
+                 cnt, md & ~M_DIST, T.heavy, nhv, T.B0, T.nB, hc);
       P.end(k == 1 ? PC_TILE_DOWN : PC_MID_DOWN);
     } else {
       if (T.k0 == 1 && !dist && h.wdown_grid > 0)
@@ -2618,7 +2714,7 @@ void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q
            (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(), (const int32_t*)h.long_rows.p,
            (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1,
-           (const double*)nullptr, (const double*)nullptr, (double*)nullptr);
+           (const double*)nullptr, (const double*)nullptr, (double*)nullptr, h.nmed);
   };
   if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true>);
@@ -2639,7 +2735,7 @@ void launch_spmv_sep(Handle& h, const double* z, const double* pold, double* pne
              (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
              (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
              (const double2*)nullptr, (double*)nullptr, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1, z, pold,
-             pnew);
+             pnew, h.nmed);
   };
   if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true, true>);

@@ -348,6 +348,39 @@ def test_full_size_config1_apply_R_and_pcg():
     assert np.linalg.norm(r - L @ x) <= 2e-8 * np.linalg.norm(r)
 
 
+@pytest.mark.parametrize("chunk", [2, 37, 256])
+def test_heavy_aggregate_chunks(chunk, monkeypatch):
+    """Power-law hub aggregates (hundreds of children) cut into chunks of a
+    CTA each (MSP_HEAVY_CHUNK: several chunks per aggregate, a ragged last
+    one; the up sweep's per-chunk partials summed by the last-arriving
+    chunk): hierarchy bit-exact, apply_R within 1e-12 of the refined oracle
+    reference, PCG as test_pcg_msp; the medium (8 lanes per row), long and
+    huge SpMV rows of the same graph against apply_L at 1e-12."""
+    monkeypatch.setenv("MSP_HEAVY_CHUNK", str(chunk))
+    g = G.chung_lu(30000, 2.1, 16.0, 7)
+    seed = 11
+    h = A.build_hierarchy(g, seed)
+    s = gpu_setup(g, 0.8, 0, seed)
+    assert list(s.level_sizes()) == h.sizes
+    x = np.random.default_rng(1).standard_normal(g.n)
+    assert relmax(s.apply_L(dt(x)).cpu().numpy(), GR.apply_L(g, x)) <= 1e-12
+    sysm = E.expand_msp_only(g, h, 0.8)
+    r = G.rhs(g.n, 3)
+    apply_R_bar(f"chung_lu_30000/chunk{chunk}", s.apply_R(dt(r)).cpu().numpy(), sysm, r)
+    L = GR.laplacian_of_graph(g)
+    b = G.rhs(g.n, 4)
+    ref = PC.pcg(lambda v: L @ v, b, PR.msp(sysm), 1e-8, 20000)
+    out = s.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    assert out["converged"] == 1 and ref.converged
+    d = abs(out["iterations"] - ref.iterations)
+    if d > 2:
+        assert d <= iteration_band(L, b, sysm, ref.iterations)
+    e = out["x"].cpu().numpy() - ref.x
+    e -= e.mean()
+    xs = ref.x - ref.x.mean()
+    assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs))
+
+
 FULL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full_size")
 
 
