@@ -479,7 +479,7 @@ void dist_iteration(DistGroup& g, Prof* const* P) {
                                                            h.counters.p);
     MSP_LAUNCH_CHECK();
     P[i]->begin();
-    if (pairs) launch_spmv_pairs(h, zin[i], zout[i], h.vq.p, h.vx.p, g.st, d.row0, d.row1);
+    if (pairs) launch_spmv_pairs(h, zin[i], zout[i], h.vq.p, h.vx.p, g.st, d.row0, d.row1, false);
     else if (use_sep(h)) launch_spmv_sep(h, zin[i], pold[i], pnew[i], h.vq.p, h.vx.p, g.st, d.row0, d.row1);
     else launch_spmv<true>(h, zin[i], pold[i], pnew[i], h.vq.p, h.vx.p, g.st, d.row0, d.row1);
     P[i]->end(PC_SPMV);

@@ -149,13 +149,21 @@ struct Handle {
   DBuf<double> sell_w;
   DBuf<uint32_t> sell_mask;
   DBuf<int32_t> long_rows;
+  // hot-vertex gather cache (power-law graphs): the nhot highest-degree rows
+  // (hot_rows, by decreasing degree), their (z, p) pairs copied each
+  // iteration into hot_pairs (L2-resident), and column copies in which a hot
+  // column j reads HOT_BIT | rank(j)
+  int64_t nhot = 0;
+  DBuf<int32_t> hot_rows, sell_colh, col1h;
+  DBuf<double> hot_pairs;
   // huge rows cut into segments (sched.cuh HugeDesc)
   DBuf<int4> hseg;
   DBuf<int32_t> hfirst;
   DBuf<unsigned> hcnt;
   DBuf<double> hpart;
   int64_t nhseg = 0;
-  HugeDesc huge_desc() const { return HugeDesc{hseg.p, nhseg, hfirst.p, hcnt.p, hpart.p}; }
+  DBuf<double> hdot;
+  HugeDesc huge_desc() const { return HugeDesc{hseg.p, nhseg, hfirst.p, hcnt.p, hpart.p, hdot.p, nhuge}; }
 
   // ---- solve schedule: tiers of tile
   // kernels over levels 1..Kc, then one single-CTA kernel for Kc..L
@@ -257,6 +265,7 @@ void add_into(Handle& h, const double* a, double* y, cudaStream_t st);
 void alloc_solve_workspace(Handle& h);
 void build_schedule(Handle& h, cudaStream_t st);   // setup.cu: tiers, tiles, Kc
 void build_heavy_chunks(Handle& h, cudaStream_t st);  // setup.cu: chunks of the heavy aggregates
+void build_hot_cache(Handle& h, cudaStream_t st);     // setup.cu: hot-vertex gather cache
 // pegp.cu
 void pegp_build(Handle& h, cudaStream_t st);
 void apply_LH_nested(Handle& h, const double* x, double* y, cudaStream_t st);

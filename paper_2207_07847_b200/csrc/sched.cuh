@@ -21,6 +21,7 @@ constexpr int MAXL = 40;   // levels
 // the CTA that finishes a row's last segment (ticket cnt[row]) sums the
 // row's partials in segment order (deterministic) and writes the row.
 constexpr int HUGE_SEG = 16384;
+constexpr int32_t HOT_BIT = 1 << 30;  // column flag: read the hot-vertex cache (rank in the low bits)
 constexpr int MED_ROW = 64;  // medium rows (lcap < degree <= MED_ROW): 8 lanes per row in the SpMV
 struct HugeDesc {
   const int4* seg;       // [nseg]: x = huge-row index (into long_rows[nlong + x]), y = e0, z = e1
@@ -28,6 +29,9 @@ struct HugeDesc {
   const int32_t* first;  // [nhuge + 1]: first segment of each huge row
   unsigned* cnt;         // [nhuge]: arrival tickets (zero between launches)
   double* part;          // [nseg]: segment partial sums
+  double* dot;           // [nhuge]: the row's p_i (L p)_i, added to (p, q) in row order by the
+                         // SpMV's last block (which CTA finishes a row varies run to run)
+  int64_t nhuge;
 };
 constexpr int MAXT = 16;   // levels per tier
 

@@ -1085,6 +1085,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
       h.hfirst.alloc(h.nhuge + 1);
       h.hcnt.alloc(std::max<int64_t>(h.nhuge, 1));
       h.hpart.alloc(std::max<size_t>(segs.size(), 1));
+      h.hdot.alloc(std::max<int64_t>(h.nhuge, 1));
       if (!segs.empty())
         MSP_CUDA(cudaMemcpyAsync(h.hseg.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
       MSP_CUDA(cudaMemcpyAsync(h.hfirst.p, first.data(), first.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -1093,6 +1094,7 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
     }
   }
 
+  build_hot_cache(h, st);
   clk.mark(st, "SELL");
   // ---- top level: dense pseudo-inverse of sigma_l L_l
   {
@@ -1262,6 +1264,71 @@ std::vector<int4> make_tile_segs(const Handle& h, int k0_, int nl, const TierDes
   return segs;
 }
 
+__global__ void k_deg_key(int64_t n, const int32_t* __restrict__ rowptr, int32_t maxdeg, int32_t* __restrict__ key) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) key[i] = maxdeg - (rowptr[i + 1] - rowptr[i]);  // ascending key = decreasing degree
+}
+
+__global__ void k_hot_rank(int64_t nhot, const int32_t* __restrict__ rows, int32_t* __restrict__ rank) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < nhot) rank[rows[k]] = (int32_t)k;
+}
+
+__global__ void k_remap_cols(int64_t m, const int32_t* __restrict__ col, const int32_t* __restrict__ rank,
+                             int32_t* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < m) {
+    const int32_t j = col[e];
+    const int32_t r = rank[j];
+    out[e] = (r >= 0) ? (HOT_BIT | r) : j;
+  }
+}
+
+// Hot-vertex gather cache of a heavy-tailed graph (long rows present, n
+// large): in a Chung-Lu graph of exponent 2.1 the few highest-degree
+// vertices are the endpoints of most edges, but the nested numbering
+// scatters them over the whole (z, p) array, so at configs[4]'s full size
+// (47M vertices, a 757 MB pair array) the SpMV's gathers missed L2 83 % of
+// the time (57.7 GB of DRAM reads per SpMV for 10 GB of streams).  Their
+// pairs are copied each iteration into one compact array (16 B each) that
+// stays in L2, and the SpMV's column copies address it directly.  The
+// copied values are the same doubles: the SpMV result is unchanged bit for
+// bit.  MSP_HOT_K sets the count (0: off).
+void build_hot_cache(Handle& h, cudaStream_t st) {
+  h.nhot = 0;
+  const int64_t n = h.n;
+  int64_t K = 0;
+  if (h.nlong + h.nhuge > 0 && n >= (int64_t(1) << 23)) K = int64_t(1) << 22;  // 64 MB of pairs
+  if (const char* e = std::getenv("MSP_HOT_K")) K = std::atoll(e);
+  K = std::min<int64_t>(K, n);
+  if (K <= 0) return;
+  Temp tmp;
+  DBuf<int> md;
+  md.alloc(1);
+  MSP_CUDA(cudaMemsetAsync(md.p, 0, sizeof(int), st));
+  k_max_degree<<<grid_for(n), TPB, 0, st>>>(n, h.rowptr1.p, md.p);
+  const int maxdeg = d2h_scalar(md.p, st);
+  DBuf<int32_t> key, skey, ids, sids, rank;
+  key.alloc(n); skey.alloc(n); ids.alloc(n); sids.alloc(n); rank.alloc(n);
+  k_deg_key<<<grid_for(n), TPB, 0, st>>>(n, h.rowptr1.p, maxdeg, key.p);
+  k_iota32<<<grid_for(n), TPB, 0, st>>>(n, ids.p);
+  sort_pairs(tmp, key.p, skey.p, ids.p, sids.p, n, bits_for((uint64_t)maxdeg + 1), st);  // stable: ties by id
+  h.nhot = K;
+  h.hot_rows.alloc(K);
+  MSP_CUDA(cudaMemcpyAsync(h.hot_rows.p, sids.p, K * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  MSP_CUDA(cudaMemsetAsync(rank.p, 0xff, n * sizeof(int32_t), st));
+  k_hot_rank<<<grid_for(K), TPB, 0, st>>>(K, h.hot_rows.p, rank.p);
+  const int64_t ms = h.sell_ptr.n ? d2h_scalar(h.sell_ptr.p + h.nslices, st) : 0;
+  h.sell_colh.alloc(std::max<int64_t>(ms, 1));
+  if (ms) k_remap_cols<<<grid_for(ms), TPB, 0, st>>>(ms, h.sell_col.p, rank.p, h.sell_colh.p);
+  h.col1h.alloc(std::max<int64_t>(h.nnz_adj, 1));
+  k_remap_cols<<<grid_for(h.nnz_adj), TPB, 0, st>>>(h.nnz_adj, h.col1.p, rank.p, h.col1h.p);
+  h.hot_pairs.alloc(2 * K + 8);
+  MSP_CUDA(cudaMemsetAsync(h.hot_pairs.p, 0, (2 * K + 8) * sizeof(double), st));
+  MSP_LAUNCH_CHECK();
+  MSP_CUDA(cudaStreamSynchronize(st));
+}
+
 // K_j = sum over the leftovers x of heavy aggregate h of C(x, j) N_x (one
 // CTA per heavy aggregate, fixed-order block sum; setup only)
 __global__ void k_heavy_const(int64_t nh, const int32_t* __restrict__ heavy, const int32_t* __restrict__ cp,
@@ -1292,7 +1359,7 @@ void build_heavy_chunks(Handle& h, cudaStream_t st) {
   const int L = h.levels;
   h.hch_off.assign(L, 0);
   const int64_t nh = h.heavy_off.empty() ? 0 : h.heavy_off[L - 1];
-  if (nh == 0) { h.hch_off.clear(); return; }
+  if (nh == 0 || std::getenv("MSP_NO_HEAVY_CHUNKS")) { h.hch_off.clear(); return; }  // off: a CTA per heavy aggregate
   int64_t CH = HEAVY_CHUNK;  // MSP_HEAVY_CHUNK: smaller chunks for tests of the multi-chunk path
   if (const char* e = std::getenv("MSP_HEAVY_CHUNK")) CH = std::max<int64_t>(2, std::atoll(e));
   std::vector<int4> segs;

@@ -375,6 +375,18 @@ __device__ __forceinline__ bool huge_last(const HugeDesc& hd, int hr, int64_t s,
   return true;
 }
 
+// (p, q) terms of the huge rows (one warp, fixed row order; a distributed
+// rank's own rows only)
+__device__ __forceinline__ double huge_dot_sum(const HugeDesc& hd, const int32_t* __restrict__ long_rows,
+                                              int64_t nlong, int64_t row0, int64_t row1) {
+  double a = 0.0;
+  for (int64_t i = threadIdx.x & 31; i < hd.nhuge; i += 32) {
+    const int64_t r = long_rows[nlong + i];
+    if (r >= row0 && r < row1) a += __ldcg(hd.dot + i);
+  }
+  return warp_sum(a);
+}
+
 // PCG scalars after the level-1 output: rz = (r, R r)
 __device__ __forceinline__ void finish_rz(double rz, double* scal, int mode) {
   if (mode == M_ITER) scal[S_BETA] = rz / scal[S_RHO];
@@ -494,7 +506,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
       if (PCG) {
         pnew[r] = pi;
         x[r] += alpha * po;
-        d += pi * tot;
+        hd.dot[sg.x] = pi * tot;  // summed in row order at the end
       }
     }
   }
@@ -504,7 +516,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
   if (threadIdx.x < 32) {  // only warp 0 waits on the ticket
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
     if (warp_last_block(&cnt[C_SPMV])) {
-      const double pq = warp_sum_partials(part, gridDim.x);
+      const double pq = warp_sum_partials(part, gridDim.x) + huge_dot_sum(hd, long_rows, nlong, row0, row1);
       if (threadIdx.x == 0) {
         scal[S_PQ] = pq;
         scal[S_ALPHA] = scal[S_RHO] / pq;
@@ -520,7 +532,18 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_MINB) k_spmv(int64_t n, int64_t 
 // column / weight / row vectors of s+1 are already in flight.
 #undef TRACE_KID
 #define TRACE_KID 6
-template <int MW, bool UNIF, bool SEP = false>
+// hot-vertex cache fill (power-law graphs, setup.cu build_hot_cache): the
+// (z, p_old) pairs of the nhot highest-degree rows, copied into one compact
+// L2-resident array before the SpMV gathers them
+__global__ void k_hot_gather(int64_t nhot, const int32_t* __restrict__ rows, const double2* __restrict__ zp,
+                             double2* __restrict__ hot, const unsigned* __restrict__ cnt) {
+  pdl_wait();
+  if (cnt[C_DONE]) return;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nhot; k += (int64_t)gridDim.x * blockDim.x)
+    hot[k] = zp[rows[k]];
+}
+
+template <int MW, bool UNIF, bool SEP = false, bool HOT = false>
 __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64_t nslices, const int64_t* __restrict__ sptr,
                                                       const int32_t* __restrict__ scol, const double* __restrict__ sw,
                                                       const uint32_t* __restrict__ smask, int64_t nlong, const HugeDesc hd,
@@ -532,7 +555,8 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
                                                       double* __restrict__ part, double* __restrict__ scal,
                                                       unsigned int* __restrict__ cnt, int64_t row0, int64_t row1,
                                                       const double* __restrict__ zs, const double* __restrict__ ps,
-                                                      double* __restrict__ pn, int64_t nmed) {
+                                                      double* __restrict__ pn, int64_t nmed,
+                                                      const double2* __restrict__ hot) {
   // pairs (!SEP): zp[i] = (z_i, p_old_i), the new p_i goes to zpout[2 i + 1];
   // SEP: z, p_old and the new p in three plain vectors zs, ps, pn (every
   // store a full sector: no L2 fill of a half-written pair line).  Rows
@@ -540,6 +564,11 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   auto zpj = [&](int64_t j) -> double2 {
     if (SEP) return make_double2(zs[j], ps[j]);
     return zp[j];
+  };
+  // a gathered neighbour: HOT columns with HOT_BIT read the cache
+  auto zpg = [&](int32_t j) -> double2 {
+    if (HOT && (j & HOT_BIT)) return hot[j & (HOT_BIT - 1)];
+    return zpj(j);
   };
   auto put_p = [&](int64_t r, double v) {
     if (SEP) pn[r] = v;
@@ -624,7 +653,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
 #pragma unroll
     for (int k = 0; k < MW; ++k)
       if (k < wd) {
-        const double2 v = zpj(jc[k]);
+        const double2 v = zpg(jc[k]);
         g[k] = v.x + beta * v.y;
       }
     double acc = 0.0;
@@ -662,7 +691,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
         pi = vr.x + beta * pr;
         if (sub == 0) xr = x[r];
         acc = row_dot<MG>(col, w, rowptr[r], rowptr[r + 1], sub, pi, [&](int32_t j) {
-          const double2 v = zpj(j);
+          const double2 v = zpg(j);
           return v.x + beta * v.y;
         });
       }
@@ -684,7 +713,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     const double pi = vr.x + beta * pr;
     const double xr = (lane == 0) ? x[r] : 0.0;  // in flight with the row
     double acc = row_dot<32>(col, w, rowptr[r], rowptr[r + 1], lane, pi, [&](int32_t j) {
-      const double2 v = zpj(j);
+      const double2 v = zpg(j);
       return v.x + beta * v.y;
     });
     acc = warp_sum(acc);
@@ -703,7 +732,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     const double pr = vr.y;
     const double pi = vr.x + beta * pr;
     double acc = row_dot<TPB>(col, w, sg.y, sg.z, threadIdx.x, pi, [&](int32_t j) {
-      const double2 v = zpj(j);
+      const double2 v = zpg(j);
       return v.x + beta * v.y;
     });
     acc = block_sum<TPB>(acc);
@@ -712,7 +741,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
       q[row] = tot;
       put_p(row, pi);
       x[row] += alpha * pr;
-      d += pi * tot;
+      hd.dot[sg.x] = pi * tot;  // summed in row order at the end
     }
   }
   TRACE(2);
@@ -721,7 +750,7 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
     if (warp_last_block(&cnt[C_SPMV])) {
-      const double pq = warp_sum_partials(part, gridDim.x);
+      const double pq = warp_sum_partials(part, gridDim.x) + huge_dot_sum(hd, long_rows, nlong, row0, row1);
       if (threadIdx.x == 0) {
         scal[S_PQ] = pq;
         scal[S_ALPHA] = scal[S_RHO] / pq;
@@ -2707,16 +2736,32 @@ void launch_spmv(Handle& h, const double* z, const double* pold, double* pnew, d
 
 // SpMV of the MSP iteration on interleaved (z, p) pairs (M_ZS2)
 void launch_spmv_pairs(Handle& h, const double* zp_in, double* zp_out, double* q, double* x, cudaStream_t st,
-                       int64_t row0 = 0, int64_t row1 = -1) {
+                       int64_t row0 = 0, int64_t row1 = -1, bool hot_ok = true) {
   if (row1 < 0) row1 = h.n;
+  const bool hot = hot_ok && h.nhot > 0;
+  if (hot) {
+    launch_c(16, k_hot_gather, (unsigned)std::min<int64_t>(grid_for(h.nhot), 148 * 8), TPB, 0, st, h.nhot,
+             (const int32_t*)h.hot_rows.p, reinterpret_cast<const double2*>(zp_in),
+             reinterpret_cast<double2*>(h.hot_pairs.p), (const unsigned*)h.counters.p);
+    ++h.launches;
+  }
+  const int32_t* sc = hot ? h.sell_colh.p : h.sell_col.p;
+  const int32_t* cc = hot ? h.col1h.p : h.col1.p;
   auto go = [&](auto kern) {
-    launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, (const int32_t*)h.sell_col.p,
+    launch_c(2, kern, h.spmv_grid, TPB, 0, st, h.n, h.nslices, (const int64_t*)h.sell_ptr.p, sc,
            (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(), (const int32_t*)h.long_rows.p,
-           (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
+           (const int32_t*)h.rowptr1.p, cc, (const double*)h.w1.p,
            reinterpret_cast<const double2*>(zp_in), zp_out, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1,
-           (const double*)nullptr, (const double*)nullptr, (double*)nullptr, h.nmed);
+           (const double*)nullptr, (const double*)nullptr, (double*)nullptr, h.nmed,
+           reinterpret_cast<const double2*>(h.hot_pairs.p));
   };
-  if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
+  if (hot) {
+    if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true, false, true>);
+    else if (h.sell_uniform && h.sell_maxw == 8) go(k_spmv_pipe<8, true, false, true>);
+    else if (h.sell_maxw <= 4) go(k_spmv_pipe<4, false, false, true>);
+    else if (h.sell_maxw <= 8) go(k_spmv_pipe<8, false, false, true>);
+    else go(k_spmv_pipe<16, false, false, true>);
+  } else if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true>);
   else if (h.sell_uniform && h.sell_maxw == 8) go(k_spmv_pipe<8, true>);
   else if (h.sell_maxw <= 4) go(k_spmv_pipe<4, false>);
@@ -2735,7 +2780,7 @@ void launch_spmv_sep(Handle& h, const double* z, const double* pold, double* pne
              (const double*)h.sell_w.p, (const uint32_t*)h.sell_mask.p, h.nlong, h.huge_desc(),
              (const int32_t*)h.long_rows.p, (const int32_t*)h.rowptr1.p, (const int32_t*)h.col1.p, (const double*)h.w1.p,
              (const double2*)nullptr, (double*)nullptr, q, x, h.red.p, h.scal.p, h.counters.p, row0, row1, z, pold,
-             pnew, h.nmed);
+             pnew, h.nmed, (const double2*)nullptr);
   };
   if (h.sell_uniform && h.sell_maxw == 4) go(k_spmv_pipe<4, true, true>);
   else if (h.sell_uniform && h.sell_maxw == 6) go(k_spmv_pipe<6, true, true>);
@@ -2907,6 +2952,9 @@ void alloc_solve_workspace(Handle& h) {
   int64_t need = std::max<int64_t>({(int64_t)h.spmv_grid, (int64_t)grid_for(h.n), 1});
   for (auto& T : h.tiers) need = std::max<int64_t>(need, T.ntiles);
   if (h.lv.size() > 1) need = std::max<int64_t>(need, grid_for(h.lv[1].n));
+  // generic level-1 down kernel: a block per 256 parents plus a CTA per heavy
+  // aggregate or per heavy chunk, each with an (r, R r) partial
+  need += (h.hch_off.empty() ? 0 : h.hch_off.back()) + (h.heavy_off.empty() ? 0 : h.heavy_off.back());
   h.red_cap = 4 * need + 64;
   h.red.alloc(h.red_cap);
   MSP_CUDA(cudaMemset(h.red.p, 0, h.red_cap * sizeof(double)));

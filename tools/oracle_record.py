@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--perturb", type=int, default=0)
     ap.add_argument("--mu", type=float, default=0.8)
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "full_size"))
+    ap.add_argument("--apply-l", default="csr", choices=["csr", "incidence"],
+                    help="L p as the assembled CSR Laplacian (default) or as B^T W B p (oracle.graph.apply_L, "
+                         "the definition with the exact diagonal)")
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
     t0 = time.time()
@@ -51,9 +54,15 @@ def main():
         b = b * (1 + 1e-15 * np.random.default_rng(args.perturb).standard_normal(b.size))
     print(f"setup {time.time() - t0:.1f}s n={g.n} levels={h.nlevels}", flush=True)
     t0 = time.time()
-    res = PC.pcg(lambda v: L @ v, b, R, 1e-8, 100000)
+    if args.apply_l == "incidence":
+        B = GR.incidence(g.n, g.u, g.v).tocsr()
+        BT = B.T.tocsr()
+        res = PC.pcg(lambda v: BT @ (g.w * (B @ v)), b, R, 1e-8, 100000)
+    else:
+        res = PC.pcg(lambda v: L @ v, b, R, 1e-8, 100000)
     print(f"pcg {time.time() - t0:.1f}s iterations={res.iterations} converged={res.converged}", flush=True)
-    name = f"cfg{args.config}_pcg_msp" + (f"_p{args.perturb}" if args.perturb else "") + ".npz"
+    name = (f"cfg{args.config}_pcg_msp" + (f"_p{args.perturb}" if args.perturb else "")
+            + ("_inc" if args.apply_l == "incidence" else "") + ".npz")
     kw = dict(iterations=res.iterations, converged=res.converged, resnorms=np.array(res.resnorms),
               mu=args.mu, rhs_seed=4, hierarchy_seed=0)
     if not args.perturb:
