@@ -1069,10 +1069,12 @@ void build_setup(Handle& h, const int64_t* rowptr_d, const int32_t* col_d, const
       }
       std::vector<int4> segs;
       std::vector<int32_t> first(h.nhuge + 1, 0);
+      int64_t hseg = HUGE_SEG;  // MSP_HUGE_SEG: shorter segments for tests of the multi-segment path
+      if (const char* e = std::getenv("MSP_HUGE_SEG")) hseg = std::max<int64_t>(32, std::atoll(e));
       for (int64_t i = 0; i < h.nhuge; ++i) {
         first[i] = (int32_t)segs.size();
-        for (int64_t e = hp[2 * i]; e < hp[2 * i + 1]; e += HUGE_SEG)
-          segs.push_back(make_int4((int)i, (int)e, (int)std::min<int64_t>(e + HUGE_SEG, hp[2 * i + 1]), 0));
+        for (int64_t e = hp[2 * i]; e < hp[2 * i + 1]; e += hseg)
+          segs.push_back(make_int4((int)i, (int)e, (int)std::min<int64_t>(e + hseg, hp[2 * i + 1]), 0));
       }
       first[h.nhuge] = (int32_t)segs.size();
       h.nhseg = (int64_t)segs.size();

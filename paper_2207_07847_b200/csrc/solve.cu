@@ -307,7 +307,7 @@ __device__ __forceinline__ double2 warp_sum_partials2(const double* pa, const do
 // s0+1, leftovers s0+2..), K(j) the packed K'^{-1} (uu, uv, vv), C(p, j) the
 // leftover coefficients (sigma w_xu / d, sigma w_xv / d, 1 / d):
 // zeta = K_S^{-1} t, emitted as ef(p, z_B + zeta_p, z_B + zeta_p + wbm).
-template <typename I, typename TF, typename KF, typename CF, typename EF>
+template <int UNR = 1, typename I, typename TF, typename KF, typename CF, typename EF>
 __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, double wbm, TF tf, EF ef) {
   const double kuu = K(0), kuv = K(1), kvv = K(2);
   const double tu = tf(s0), tv = tf(s0 + 1);
@@ -318,7 +318,7 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
     return;
   }
   double au = tu, av = tv;
-  #pragma unroll 1
+  #pragma unroll UNR
   for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     au += C(p, 0) * tx;
@@ -327,7 +327,7 @@ __device__ __forceinline__ void block_solve(I s0, I s1, KF K, CF C, double zb, d
   const double zu = kuu * au + kuv * av, zv = kuv * au + kvv * av;
   { const double z = zb + zu; ef(s0, z, z + wbm); }
   { const double z = zb + zv; ef(s0 + 1, z, z + wbm); }
-  #pragma unroll 1
+  #pragma unroll UNR
   for (I p = s0 + 2; p < s1; ++p) {
     const double tx = tf(p);
     const double zx = C(p, 2) * tx + C(p, 0) * zu + C(p, 1) * zv;
@@ -345,16 +345,19 @@ template <int S, typename PJ>
 __device__ __forceinline__ double row_dot(const int32_t* __restrict__ col, const double* __restrict__ w, int32_t e0,
                                           int32_t e1, int sub, double pi, PJ pj) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  // the row's columns and weights are streamed once per product: evict-first,
+  // so the gathered vectors (and the hot-vertex cache) keep the L2
   int32_t e = e0 + sub;
   for (; e + 3 * S < e1; e += 4 * S) {
-    const int32_t j0 = col[e], j1 = col[e + S], j2 = col[e + 2 * S], j3 = col[e + 3 * S];
-    const double w0 = w[e], w1 = w[e + S], w2 = w[e + 2 * S], w3 = w[e + 3 * S];
+    const int32_t j0 = __ldcs(col + e), j1 = __ldcs(col + e + S), j2 = __ldcs(col + e + 2 * S),
+                  j3 = __ldcs(col + e + 3 * S);
+    const double w0 = __ldcs(w + e), w1 = __ldcs(w + e + S), w2 = __ldcs(w + e + 2 * S), w3 = __ldcs(w + e + 3 * S);
     a0 += w0 * (pi - pj(j0));
     a1 += w1 * (pi - pj(j1));
     a2 += w2 * (pi - pj(j2));
     a3 += w3 * (pi - pj(j3));
   }
-  for (; e < e1; e += S) a0 += w[e] * (pi - pj(col[e]));
+  for (; e < e1; e += S) a0 += __ldcs(w + e) * (pi - pj(__ldcs(col + e)));
   return (a0 + a1) + (a2 + a3);
 }
 
@@ -566,8 +569,16 @@ __global__ void __launch_bounds__(TPB, MSP_SPMV_LB) k_spmv_pipe(int64_t n, int64
     return zp[j];
   };
   // a gathered neighbour: HOT columns with HOT_BIT read the cache
+  uint64_t keep_pol = 0;
+  if (HOT) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep_pol));
   auto zpg = [&](int32_t j) -> double2 {
-    if (HOT && (j & HOT_BIT)) return hot[j & (HOT_BIT - 1)];
+    if (HOT && (j & HOT_BIT)) {  // the hot-vertex cache, kept resident in L2 (evict-last)
+      double2 v;
+      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                   : "=d"(v.x), "=d"(v.y)
+                   : "l"(hot + (j & (HOT_BIT - 1))), "l"(keep_pol));
+      return v;
+    }
     return zpj(j);
   };
   auto put_p = [&](int64_t r, double v) {
@@ -2129,7 +2140,7 @@ __global__ void __launch_bounds__(TPB) k_down_lvl(const __grid_constant__ Lv lv,
     if (B < B0 + nB && cp[B + 1] - cp[B] <= HEAVY_AGG) {
       const double* ki = kinv + 3 * (lv.off[k] - lv.n[0] + B);
       const int64_t lb = 3 * (lv.lo[k - 1] - 2 * B - 2);
-      block_solve(
+      block_solve(  // (an unrolled leftover loop measured slower on configs[4]: 1.26 -> 1.32 ms)
           cp[B], cp[B + 1], [&](int j) { return ki[j]; }, [&](int64_t p, int j) { return lof[lb + 3 * p + j]; },
           zB[B], lv.negmu * wB[B], tf, ef);
     }

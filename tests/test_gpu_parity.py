@@ -399,6 +399,36 @@ def test_hot_vertex_cache_bit_identical(monkeypatch):
     assert torch.equal(outs[0]["x"], outs[1]["x"])
 
 
+def test_huge_rows_multi_segment_reproducible(monkeypatch):
+    """Rows above MSP_SELL_HUGE entries are cut into segments of a CTA each
+    (the last-arriving CTA adds the partials in segment order); with many
+    multi-segment rows the SpMV matches apply_L's definition at 1e-12, and
+    PCG is bit-reproducible run to run -- the huge rows' (p, q) terms are
+    added in row order, not by whichever CTA finishes a row."""
+    monkeypatch.setenv("MSP_SELL_HUGE", "200")
+    monkeypatch.setenv("MSP_HUGE_SEG", "64")
+    g = G.chung_lu(30000, 2.1, 16.0, 7)
+    s = gpu_setup(g, 0.8, 0, 11)
+    x = np.random.default_rng(1).standard_normal(g.n)
+    assert relmax(s.apply_L(dt(x)).cpu().numpy(), GR.apply_L(g, x)) <= 1e-12
+    b = G.rhs(g.n, 4)
+    o1 = s.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    o2 = s.pcg_solve(dt(b), rtol=1e-8, maxit=20000)
+    assert o1["converged"] == 1 and o1["iterations"] == o2["iterations"]
+    assert torch.equal(o1["x"], o2["x"])
+    h = A.build_hierarchy(g, 11)
+    sysm = E.expand_msp_only(g, h, 0.8)
+    L = GR.laplacian_of_graph(g)
+    ref = PC.pcg(lambda v: L @ v, b, PR.msp(sysm), 1e-8, 20000)
+    d = abs(o1["iterations"] - ref.iterations)
+    if d > 2:
+        assert d <= iteration_band(L, b, sysm, ref.iterations)
+    e = o1["x"].cpu().numpy() - ref.x
+    e -= e.mean()
+    xs = ref.x - ref.x.mean()
+    assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs))
+
+
 FULL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full_size")
 
 
