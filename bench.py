@@ -168,23 +168,30 @@ class OracleWorkload:
     """The oracle (as it stands) on a bounded sample of the workload; setup
     is untimed."""
 
-    def __init__(self, cfg: int, mu: float, log):
+    def __init__(self, cfg: int, mu: float, log, precond: str = "msp"):
         from inputs import graphs as G
         from oracle import aggregation as A, expansion as E, graph as GR, precond as PR
         t0 = time.time()
         self.scale = SAMPLE_SCALE.get(cfg, 0.25)
+        self.precond = precond
         self.g = G.config_graph(cfg, self.scale)
         h = A.build_hierarchy(self.g, 0)
-        self.R = PR.msp(E.expand_msp_only(self.g, h, mu))
+        if precond == "pegp":
+            self.R = PR.pegp(E.expand(self.g, h, mu))
+        elif precond == "none":
+            self.R = lambda v: v
+        else:
+            self.R = PR.msp(E.expand_msp_only(self.g, h, mu))
         self.L = GR.laplacian_of_graph(self.g)
         self.b = G.rhs(self.g.n, 0)
         log(f"oracle setup {time.time() - t0:.1f}s (sample: configs[{cfg}] at scale {self.scale}, n={self.g.n})")
         self.one = None
 
     def describe(self, cfg):
+        solver = {"msp": "SuperLU solve of L_T~", "pegp": "SuperLU solve of L_H~", "none": "no preconditioner"}
         return (f"configs[{cfg}] family at linear scale {self.scale} (n={self.g.n}, nnz(L)={self.g.nnz_laplacian}): "
-                "PCG-MSP iterations of the oracle (scipy SpMV + SuperLU solve of L_T~), one process per host "
-                "core, all on the same sample; oracle setup untimed")
+                f"PCG-{self.precond.upper()} iterations of the oracle (scipy SpMV + {solver[self.precond]}), one "
+                "process per host core, all on the same sample; oracle setup untimed")
 
     def _iters(self, iters):
         from oracle import pcg as PC
@@ -238,7 +245,7 @@ def run_reference(args, rank):
     if rank != 0:
         return 0
     log = lambda m: print(f"[bench/reference] {m}", file=sys.stderr, flush=True)
-    wl = OracleWorkload(args.config, args.mu, log)
+    wl = OracleWorkload(args.config, args.mu, log, args.precond)
     cores = host_cores()
     per_step = max(2.0, 90.0 / max(1, args.steps + args.warmup))
     vals = []
@@ -292,7 +299,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--precond", default="msp", choices=["msp", "none"])
+    ap.add_argument("--precond", default="msp", choices=["msp", "none", "pegp"])
+    ap.add_argument("--inner-rtol", type=float, default=1e-13, help="PEGP: inner CG relative residual (R13)")
     ap.add_argument("--mu", type=float, default=0.8)
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=200000)
@@ -343,6 +351,11 @@ def main():
     S = M.setup(n, rp, col, val, mu=args.mu, seed=0)
     del rp, col, val
     info = S.info()
+    pinfo = None
+    if args.precond == "pegp":
+        S.pegp_params(args.inner_rtol, 200000, 0)
+        pinfo = S.pegp_info()
+        log(f"PEGP: H~ nnz {pinfo['hnnz']}, build {pinfo['build_ms']:.1f} ms, coarse level {pinfo['coarse_level']}")
     log(f"setup {info['setup_ms']:.1f} ms (wall {time.time() - t0:.1f}s) levels={info['levels']} "
         f"n~={info['n_tilde']} mwm_rounds={info['mwm_rounds']}")
     drange = None
@@ -393,6 +406,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    solve_inner = S.pegp_info()["last_solve_inner_iterations"] if args.precond == "pegp" else None
     it = int(np.median(iters))
     # partitioned: all ranks solve ONE system (strong scaling); replicas: one each (weak)
     copies = 1 if use_dist else world
@@ -423,7 +437,10 @@ def main():
     # bracketing each launch on the solve's stream; serialised, no graph)
     S.set_profiling(True)
     flush.fill_(1.0)
-    solve(b, x)
+    if args.precond == "pegp":   # one preconditioner apply (the inner CG) stands for the step's kernels
+        S.apply_R(b, precond="pegp")
+    else:
+        solve(b, x)
     S.set_profiling(False)
     prof = S.get_profile()
     sizes = S.level_sizes()
@@ -436,6 +453,10 @@ def main():
         model["tile_down"] = tile_down_bytes(sz, kt)
     if use_dist and world > 1:  # the tile byte models are whole-graph figures
         model = {"spmv": model["spmv"]}
+    if args.precond == "pegp":
+        # k_h_spmv: H~ CSR (12 B per entry) + per row: row pointer 8, row list 4,
+        # own (z, p) pair 16, q 8, p 8
+        model = {"pegp_spmv": 12 * pinfo["hnnz"] + 44 * int(info["n_tilde"])}
     hbm, peak_src = measured_peaks()
     breakdown = {}
     for k, v in prof.items():
@@ -464,7 +485,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            wl = OracleWorkload(args.config, args.mu, log)
+            wl = OracleWorkload(args.config, args.mu, log, args.precond)
             v, cit, cdt, ncores = wl.sample(15.0, host_cores())
             cpu = {"value": v, "unit": UNIT, "cores": ncores, "kind": "oracle",
                    "sample": f"{cit} iterations in {cdt:.1f}s in total; " + wl.describe(args.config)}
@@ -477,6 +498,10 @@ def main():
         extra = {"levels_built": int(info["levels"]), "n_tilde": int(info["n_tilde"]),
                  "tile_level": int(info["tile_level"]), "coarse_level": int(info["coarse_level"]),
                  "ntiles": int(info["ntiles"]), "ntiers": int(info["ntiers"])}
+        if pinfo is not None:
+            extra["pegp"] = {"inner_iterations_per_solve": solve_inner,"hnnz": pinfo["hnnz"], "build_ms": pinfo["build_ms"], "inner_rtol": args.inner_rtol,
+                             "inner_iterations_per_step": S.pegp_info()["last_inner_iterations"],
+                             "note": "inner iterations of the profiled apply; kernel_breakdown is that apply"}
         if use_dist:
             extra["partition_level"] = int(drange[2])
             extra["rank0_rows"] = int(drange[1] - drange[0])

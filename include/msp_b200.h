@@ -156,17 +156,32 @@ int msp_apply_R(msp_handle* h, int precond, const double* r, double* z, int mem,
  * entries in the canonical expanded numbering (level-k node a at
  * sum_{j<k} n_j + a, as msp_get_msp_edges), in `mem`.
  *   msp_apply_LH : y~ = L_H~ x~, the Laplacian of the PEGP H~ (§3.2,
- *                  positive edges of Eq. def:L_ell), applied matrix-free.
+ *                  positive edges of Eq. def:L_ell), in the difference form
+ *                  sum_j w_ij (x_i - x_j) over an explicit CSR of the H~ edge
+ *                  weights assembled on the GPU at the first PEGP call.
  *   msp_solve_LH : z~ = L_H~^+ r~ (minimum norm) by CG preconditioned with the
  *                  exact L_T~^+ (§3.3); *inner_iterations receives the count
- *                  (may be NULL).  Inexact: relative residual <= inner_rtol.
- *   msp_pegp_params : inner_rtol in (0, 1) (default 1e-13) and inner_maxit
- *                  (default 5000) of that CG.
+ *                  (may be NULL; refinement steps included).  Inexact:
+ *                  relative residual <= inner_rtol, then refine_steps steps
+ *                  of iterative refinement (residual in double-double).
+ *   msp_pegp_params : inner_rtol in (0, 1) (default 1e-13), inner_maxit
+ *                  (default 5000) of that CG, refine_steps in [0, 16]
+ *                  (default 0).  Applies to msp_apply_R / msp_pcg_solve with
+ *                  MSP_PRECOND_PEGP as well.
  * x and y (r and z) may not alias.  Errors: MSP_ERR_ARG, MSP_ERR_CUDA.
  */
 int msp_apply_LH(msp_handle* h, const double* x, double* y, int mem, void* stream);
 int msp_solve_LH(msp_handle* h, const double* r, double* z, int mem, void* stream, int32_t* inner_iterations);
-int msp_pegp_params(msp_handle* h, double inner_rtol, int32_t inner_maxit);
+int msp_pegp_params(msp_handle* h, double inner_rtol, int32_t inner_maxit, int32_t refine_steps);
+/*
+ * msp_pegp_info -- builds H~ if needed (on `stream`), then writes out5[5]
+ * (host): [0] nnz of the H~ edge-weight CSR (both directions), [1] inner CG
+ * iterations of the last PEGP apply / solve_LH (refinement included), [2]
+ * the level above which the inner CG's sweeps run in one CTA, [3] H~ build
+ * time in microseconds (device, CUDA events), [4] inner CG iterations of the
+ * last PCG-PEGP solve (all its applies).  Errors: MSP_ERR_ARG, MSP_ERR_CUDA.
+ */
+int msp_pegp_info(msp_handle* h, void* stream, int64_t* out5);
 
 /*
  * msp_pcg_solve -- preconditioned CG for L_G x = b, x0 = 0, stopping at the
@@ -186,8 +201,9 @@ int msp_pcg_solve(msp_handle* h, int precond, const double* b, double* x, double
  * 0 p = z + beta p fused with q = L_G p and (p, q);  1 tile up-sweep fused
  * with x/r update and (r, r);  2 per-level up-sweeps;  3 single-CTA coarse
  * kernel (coarse up-sweep, top solve, coarse down-sweep);  4 per-level
- * down-sweeps;  5 tile down-sweep with the output R r and (r, R r);  6, 7
- * unused.  msp_get_profile copies ms[MSP_PROF_NCAT] and launch counts
+ * down-sweeps;  5 tile down-sweep with the output R r and (r, R r);  6 the
+ * PEGP inner CG's fused p update + L_H~ p + (p, q) (k_h_spmv);  7 its
+ * expanded-space MSP sweeps with the x / r updates and dots.  msp_get_profile copies ms[MSP_PROF_NCAT] and launch counts
  * counts[MSP_PROF_NCAT] (host arrays) and resets them.
  */
 #define MSP_PROF_NCAT 8

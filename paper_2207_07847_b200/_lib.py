@@ -72,11 +72,13 @@ def _load():
     L.msp_get_profile.argtypes = [P, P, P]
     L.msp_apply_LH.argtypes = [P, P, P, ctypes.c_int, P]
     L.msp_solve_LH.argtypes = [P, P, P, ctypes.c_int, P, ctypes.POINTER(i32)]
-    L.msp_pegp_params.argtypes = [P, d, i32]
+    L.msp_pegp_params.argtypes = [P, d, i32, i32]
+    L.msp_pegp_info.argtypes = [P, P, P]
     L.msp_last_error.restype = ctypes.c_char_p
     for f in ("msp_setup", "msp_destroy", "msp_info", "msp_level_sizes", "msp_get_aggregates",
               "msp_get_msp_edges", "msp_apply_L", "msp_apply_R", "msp_pcg_solve", "msp_set_profiling",
-              "msp_get_profile", "msp_apply_LH", "msp_solve_LH", "msp_pegp_params"):
+              "msp_get_profile", "msp_apply_LH", "msp_solve_LH", "msp_pegp_params",
+              "msp_pegp_info"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -191,7 +193,7 @@ class Solver:
         return i, j, w
 
     PROFILE_CATEGORIES = ("spmv", "tile_up", "mid_up", "coarse", "mid_down", "tile_down",
-                          "unused6", "unused7")
+                          "pegp_spmv", "pegp_sweeps")
 
     def set_profiling(self, on: bool = True):
         _check(_lib.msp_set_profiling(self._h, 1 if on else 0))
@@ -225,8 +227,14 @@ class Solver:
     def n_tilde(self) -> int:
         return int(self.info()["n_tilde"])
 
-    def pegp_params(self, inner_rtol: float = 1e-13, inner_maxit: int = 5000):
-        _check(_lib.msp_pegp_params(self._h, float(inner_rtol), int(inner_maxit)))
+    def pegp_params(self, inner_rtol: float = 1e-13, inner_maxit: int = 5000, refine_steps: int = 0):
+        _check(_lib.msp_pegp_params(self._h, float(inner_rtol), int(inner_maxit), int(refine_steps)))
+
+    def pegp_info(self, stream=None) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        _check(_lib.msp_pegp_info(self._h, _stream_ptr(stream), out.ctypes.data))
+        return {"hnnz": int(out[0]), "last_inner_iterations": int(out[1]), "coarse_level": int(out[2]),
+                "build_ms": out[3] / 1000.0, "last_solve_inner_iterations": int(out[4])}
 
     def apply_LH(self, x, y=None, stream=None):
         """y~ = L_H~ x~ on expanded vectors (canonical expanded numbering)."""

@@ -273,12 +273,14 @@ int msp_pcg_solve(msp_handle* H, int precond, const double* b, double* x, double
   });
 }
 
-int msp_pegp_params(msp_handle* H, double inner_rtol, int32_t inner_maxit) {
+int msp_pegp_params(msp_handle* H, double inner_rtol, int32_t inner_maxit, int32_t refine_steps) {
   return guarded([&] {
     need(H != nullptr, "null handle");
-    need(inner_rtol > 0 && inner_rtol < 1 && inner_maxit > 0, "bad PEGP parameters");
+    need(inner_rtol > 0 && inner_rtol < 1 && inner_maxit > 0 && refine_steps >= 0 && refine_steps <= 16,
+         "bad PEGP parameters");
     H->h.pegp_rtol = inner_rtol;
     H->h.pegp_maxit = inner_maxit;
+    H->h.pegp_refine = refine_steps;
   });
 }
 
@@ -336,6 +338,19 @@ int msp_solve_LH(msp_handle* H, const double* r, double* z, int mem, void* strea
       it = msp::solve_LH_nested(h, rn, zn, S(stream));
     });
     if (inner_iterations) *inner_iterations = it;
+  });
+}
+
+int msp_pegp_info(msp_handle* H, void* stream, int64_t* out5) {
+  return guarded([&] {
+    need(H && out5, "null argument");
+    Handle& h = H->h;
+    msp::pegp_build(h, S(stream));
+    out5[0] = h.hnnz;
+    out5[1] = h.pegp_last_inner;
+    out5[2] = h.pegp_Kc;
+    out5[3] = (int64_t)(h.pegp_build_ms * 1000.0);
+    out5[4] = h.pegp_solve_inner;
   });
 }
 

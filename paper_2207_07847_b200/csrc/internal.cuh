@@ -15,7 +15,7 @@ namespace msp {
 
 constexpr int HEAVY_AGG = 64;
 
-enum { PC_SPMV = 0, PC_TILE_UP, PC_MID_UP, PC_COARSE, PC_MID_DOWN, PC_TILE_DOWN, PC_UNUSED6, PC_UNUSED7 };
+enum { PC_SPMV = 0, PC_TILE_UP, PC_MID_UP, PC_COARSE, PC_MID_DOWN, PC_TILE_DOWN, PC_PEGP_SPMV, PC_PEGP_SWEEPS };
 
 // ---------------------------------------------------------------- errors
 struct Error {
@@ -199,14 +199,27 @@ struct Handle {
   // ---- PEGP (built lazily on first use, pegp.cu)
   bool pegp_ready = false;
   DBuf<int32_t> parent;       // [n~]: expanded index of the parent aggregate, -1 on top
-  DBuf<int64_t> hrow;         // per-level adjacency over n~ (nested, absolute columns)
+  DBuf<int64_t> hrow;         // explicit CSR of the H~ edge weights over n~ (nested; no diagonal)
   DBuf<int32_t> hcol;
   DBuf<double> hw;
   int64_t hnnz = 0;
-  DBuf<double> ex, er, ep, eq, ez, es, ey;  // expanded-space CG vectors
-  DBuf<double> edots, epart;
+  DBuf<int32_t> hrows;        // H~ rows by degree class (short / warp / CTA rows), nested order within
+  int64_t hclass[3] = {0, 0, 0};
+  DBuf<int4> hseg2;           // long-row segments (pegp.cu HMat)
+  DBuf<int32_t> hlnseg;
+  DBuf<double> hsegpart, hlpq;
+  DBuf<unsigned> hltick;
+  int64_t hnseg = 0;
+  DBuf<double> ex, er, eq, es, ey, eres, ecor;  // expanded-space CG vectors
+  DBuf<double> ezp[2];        // (z, p) pairs of the inner CG, ping-pong
+  DBuf<double> edots, epart, eup, ezs, espmv_part;  // device scalars, block partials
+  DBuf<unsigned> etick;       // ticket counters of the inner CG
+  int pegp_Kc = 1;            // levels above pegp_Kc run in the single coarse CTA
   double pegp_rtol = 1e-13;
   int pegp_maxit = 5000;
+  int pegp_refine = 0;        // refinement steps after the inner CG (reading R13)
+  double pegp_build_ms = 0.0; // H~ assembly time (device)
+  int64_t pegp_solve_inner = 0;  // inner iterations of the last PCG-PEGP solve
   int pegp_last_inner = 0;
   DistRank* dist = nullptr;   // msp_dist_init / the loopback group
 

@@ -3139,8 +3139,10 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
     const unsigned gv = std::min<unsigned>(grid_for(n), 148u * 8u);
     launch(k_update_cg, gv, TPB, 0, st, n, h.vr.p, (const double*)nullptr, h.red.p, h.scal.p, h.counters.p,
            (int)M_INIT, 0);
+    h.pegp_solve_inner = 0;
     if (!flag()) {
       apply_R_pegp_nested(h, h.vr.p, h.vz.p, st);
+      h.pegp_solve_inner += h.pegp_last_inner;
       launch(k_rz, gv, TPB, 0, st, n, (const double*)h.vr.p, (const double*)h.vz.p, h.red.p, h.scal.p, h.counters.p,
              (int)M_INIT);
       for (int it = 0; it < maxit; ++it) {
@@ -3153,6 +3155,7 @@ void pcg_nested(Handle& h, int precond, const double* b, double* x, double rtol,
         h.launches += 2;
         if (flag()) break;
         apply_R_pegp_nested(h, h.vr.p, h.vz.p, st);
+        h.pegp_solve_inner += h.pegp_last_inner;
         launch(k_rz, gv, TPB, 0, st, n, (const double*)h.vr.p, (const double*)h.vz.p, h.red.p, h.scal.p,
                h.counters.p, (int)M_ITER);
         ++h.launches;

@@ -8,6 +8,9 @@
   the bound that residual implies.
 * apply_R PEGP and PCG with PEGP against the oracle's exact PEGP.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -40,7 +43,24 @@ GRAPHS = {
     "rgg_800": lambda: G.rgg(800, 12.0, 3),
     "chung_lu_600": lambda: G.chung_lu(600, 2.1, 16.0, 4),
     "grid3d_6": lambda: G.grid3d(6, 5, 4, seed=1),
+    # >= 10k vertices: several coarse-CTA / large-level splits of the inner CG
+    "grid_120x100_loguniform": lambda: G.grid2d(120, 100, "loguniform", 3),
+    "rgg_12000": lambda: G.rgg(12000, 12.0, 4),
 }
+
+PARITY_LOG = os.environ.get("MSP_PARITY_LOG", os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "parity_log.jsonl"))
+
+
+def record(case, quantity, err, tol):
+    """Append the achieved error and the bar applied to the parity log, then assert."""
+    try:
+        os.makedirs(os.path.dirname(PARITY_LOG), exist_ok=True)
+        with open(PARITY_LOG, "a") as f:
+            f.write(json.dumps({"case": case, "quantity": quantity, "err": err, "tol": tol}) + "\n")
+    except OSError:
+        pass
+    assert err <= tol, (case, quantity, err, tol)
 
 
 @pytest.fixture(scope="module", params=list(GRAPHS))
@@ -55,12 +75,14 @@ def case(request):
 
 def test_apply_LH(case):
     name, g, h, sysm, s = case
-    LH = sysm.LH
+    W = sysm.WH.tocsr()
     for seed in (0, 1):
         x = np.random.default_rng(seed).standard_normal(h.n_tilde)
         y = s.apply_LH(dt(x)).cpu().numpy()
-        ref = LH @ x
-        assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max(), name
+        # reference in the difference form from the oracle's H~ edge weights
+        # (R7: exact diagonal), extended precision
+        ref = np.asarray(PR._ld_laplacian_apply(W, x), dtype=np.float64)
+        record(name, "apply_LH", float(np.abs(y - ref).max() / np.abs(ref).max()), 1e-12)
 
 
 @pytest.mark.parametrize("mu", [0.3, 0.5])
@@ -79,12 +101,14 @@ def test_solve_LH(case):
     LH = sysm.LH
     r = np.random.default_rng(7).standard_normal(h.n_tilde)
     r -= r.mean()
-    s.pegp_params(1e-13, 5000)
+    # one refinement step (R13): the CG's recursively updated residual drifts
+    # from the true one over long runs; the double-double residual restores it
+    s.pegp_params(1e-13, 20000, 1)
     z, it = s.solve_LH(dt(r))
     z = z.cpu().numpy()
     assert it > 0
     res = np.linalg.norm(LH @ z - r)
-    assert res <= 2e-13 * np.linalg.norm(r), (name, res / np.linalg.norm(r), it)
+    record(name, "solve_LH_residual", float(res / np.linalg.norm(r)), 2e-13)
     assert abs(z.sum()) <= 1e-10 * np.abs(z).sum()
     zref = PR.PinvSolver(LH)(r)
     # ||z - z*|| <= ||L_H (z - z*)|| / lambda_2(L_H)
@@ -93,19 +117,29 @@ def test_solve_LH(case):
 
 
 def test_apply_R_pegp(case):
+    """apply_R PEGP at the north star's fixed 1e-12 (relative, max-norm)
+    against the oracle's refined R r (R14), with the inner CG followed by two
+    double-double refinement steps (R13)."""
     name, g, h, sysm, s = case
-    s.pegp_params(1e-14, 5000)
-    R = PR.pegp(sysm)
+    s.pegp_params(1e-13, 20000, 2)
     r = G.rhs(g.n, 8)
     z = s.apply_R(dt(r), precond="pegp").cpu().numpy()
-    zr = R(r)
-    # inner solve inexact (R13): bound from the L_H~ residual it reaches
-    assert np.abs(z - zr).max() <= 1e-9 * np.abs(zr).max(), (name, np.abs(z - zr).max() / np.abs(zr).max())
+    zr = PR.pegp_refined(sysm)(r)
+    record(name, "apply_R_pegp", float(np.abs(z - zr).max() / np.abs(zr).max()), 1e-12)
+
+
+def test_apply_R_pegp_deterministic(case):
+    name, g, h, sysm, s = case
+    s.pegp_params(1e-13, 20000, 0)
+    r = dt(G.rhs(g.n, 10))
+    z1 = s.apply_R(r, precond="pegp").cpu().numpy()
+    z2 = s.apply_R(r, precond="pegp").cpu().numpy()
+    assert np.array_equal(z1, z2), name
 
 
 def test_pcg_pegp(case):
     name, g, h, sysm, s = case
-    s.pegp_params(1e-14, 5000)
+    s.pegp_params(1e-13, 20000)
     L = GR.laplacian_of_graph(g)
     b = G.rhs(g.n, 9)
     ref = PC.pcg(lambda v: L @ v, b, PR.pegp(sysm), 1e-8, 2000)
