@@ -58,6 +58,7 @@ constexpr int H_G0 = 8;      // lanes per row of the short-row class
 constexpr int H_D0 = 32;     // short rows: degree <= H_D0
 constexpr int H_D1 = 512;    // warp rows: degree <= H_D1; longer rows: segments
 constexpr int H_SEG = 2048;  // entries per long-row segment (a CTA)
+constexpr int H_U = 4;       // short rows per 8-lane group and step
 
 inline unsigned grid_for(int64_t n, int tpb = TPB) {
   int64_t g = (n + tpb - 1) / tpb;
@@ -272,21 +273,62 @@ __device__ __forceinline__ double h_sum(int64_t e0, int64_t e1, int gsz, F&& f) 
 template <typename FV, typename TERM, typename DONE>
 __device__ __forceinline__ void h_rows(const HMat& H, FV&& fv, TERM&& term, DONE&& done) {
   const unsigned b = blockIdx.x;
-  if (b < H.b0 + H.b1) {
+  if (b < H.b0) {
+    // short rows (degree <= H_D0 = 4 x 8 lanes): every 8-lane group takes
+    // H_U rows at once so the index, row-pointer, column and gather loads of
+    // H_U rows are in flight together (the product is load-latency bound)
+    const int lane = threadIdx.x & (H_G0 - 1);
+    const int64_t per = TPB / H_G0;
+    const int64_t stride = (int64_t)H.b0 * per * H_U;
+    for (int64_t base = (int64_t)b * per * H_U; base < H.n0; base += stride) {
+      int64_t i[H_U], e0[H_U], e1[H_U];
+      double vi[H_U], acc[H_U];
+#pragma unroll
+      for (int u = 0; u < H_U; ++u) {
+        const int64_t t = base + u * per + threadIdx.x / H_G0;
+        i[u] = t < H.n0 ? H.rows[t] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < H_U; ++u) {
+        e0[u] = i[u] >= 0 ? H.row[i[u]] : 0;
+        e1[u] = i[u] >= 0 ? H.row[i[u] + 1] : 0;
+        vi[u] = i[u] >= 0 ? fv(i[u]) : 0.0;
+        acc[u] = 0.0;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < H_D0 / H_G0; ++s2) {
+#pragma unroll
+        for (int u = 0; u < H_U; ++u) {
+          const int64_t e = e0[u] + lane + s2 * H_G0;
+          if (e < e1[u]) acc[u] += term(vi[u], e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < H_U; ++u) {
+        const double a = group_sum(acc[u], H_G0);
+        if (i[u] >= 0 && lane == 0) done(i[u], vi[u], a, -1);
+      }
+    }
+    return;
+  }
+  if (b < H.b0 + H.b1) {  // grid-stride over row groups (warp-uniform trip count)
     const bool shortc = b < H.b0;
     const int gsz = shortc ? H_G0 : 32;
     const int lane = threadIdx.x & (gsz - 1);
-    const int64_t t = shortc ? (int64_t)b * (TPB / H_G0) + threadIdx.x / H_G0
-                             : (int64_t)(b - H.b0) * (TPB / 32) + threadIdx.x / 32;
-    const bool ok = shortc ? t < H.n0 : t < H.n1;
-    const int64_t i = ok ? H.rows[shortc ? t : H.n0 + t] : -1;
-    double acc = 0.0, vi = 0.0;
-    if (ok) {
-      vi = fv(i);
-      acc = h_sum(H.row[i] + lane, H.row[i + 1], gsz, [&](int64_t e) { return term(vi, e); });
+    const int64_t per = TPB / gsz, ncls = shortc ? H.n0 : H.n1, first = shortc ? 0 : H.n0;
+    const int64_t stride = (int64_t)(shortc ? H.b0 : H.b1) * per;
+    for (int64_t base = (int64_t)(shortc ? b : b - H.b0) * per; base < ncls; base += stride) {
+      const int64_t t = base + threadIdx.x / gsz;
+      const bool ok = t < ncls;
+      const int64_t i = ok ? H.rows[first + t] : -1;
+      double acc = 0.0, vi = 0.0;
+      if (ok) {
+        vi = fv(i);
+        acc = h_sum(H.row[i] + lane, H.row[i + 1], gsz, [&](int64_t e) { return term(vi, e); });
+      }
+      acc = group_sum(acc, gsz);
+      if (ok && lane == 0) done(i, vi, acc, -1);
     }
-    acc = group_sum(acc, gsz);
-    if (ok && lane == 0) done(i, vi, acc, -1);
     return;
   }
   // a segment of a long row
@@ -492,14 +534,28 @@ __device__ __forceinline__ double down_node(const ELv& lv, const EVec& v, int k,
   return rz;
 }
 
-// up sweep, aggregates of level k+1 (large levels, k + 1 <= Kc)
-__global__ void __launch_bounds__(TPB) k_e_up(ELv lv, EVec v, int k, int init, int64_t slot) {
+// one step of the up sweep: a tile tier (tstart != nullptr: a CTA per tile,
+// levels k0+1..k1 of the tile's subtree, block barriers between levels --
+// the nested numbering makes every tile a contiguous subtree, DESIGN.md "Data
+// layout") or one level (aggregates of level k0+1, a thread each)
+__global__ void __launch_bounds__(TPB) k_e_up(ELv lv, EVec v, int k0, int k1, const int32_t* __restrict__ tstart,
+                                              int64_t ntiles, int init, int64_t slot) {
   const double* sc = v.sc;
   if (sc[S::FROZEN] != 0.0) return;
   const double alpha = init ? 0.0 : sc[S::ALPHA];
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double rr = 0.0, sr = 0.0, gs = 0.0;
-  if (B < lv.n[k]) up_node(lv, v, k, B, init, alpha, rr, sr, gs);
+  if (!tstart) {
+    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < lv.n[k0]) up_node(lv, v, k0, B, init, alpha, rr, sr, gs);
+  } else {
+    const int64_t j = blockIdx.x;
+    for (int t = 1; t <= k1 - k0; ++t) {
+      const int32_t* ts = tstart + (int64_t)t * (ntiles + 1);
+      const int64_t e = ts[j + 1];
+      for (int64_t B = ts[j] + threadIdx.x; B < e; B += TPB) up_node(lv, v, k0 + t - 1, B, init, alpha, rr, sr, gs);
+      __syncthreads();
+    }
+  }
   rr = block_sum<TPB>(rr);
   sr = block_sum<TPB>(sr);
   gs = block_sum<TPB>(gs);
@@ -617,17 +673,29 @@ __global__ void __launch_bounds__(CO_T) k_e_coarse(ELv lv, EVec v, int init, int
   }
 }
 
-// down sweep, aggregates of level k+1 -> level-k children (large levels)
-__global__ void __launch_bounds__(TPB) k_e_down(ELv lv, EVec v, int k, int init, int64_t slot, int64_t nz_slots,
+// one step of the down sweep (tile tier or one level, as k_e_up), top-down;
+// the step that ends at level 1 finishes (r, z) in its last CTA
+__global__ void __launch_bounds__(TPB) k_e_down(ELv lv, EVec v, int k0, int k1, const int32_t* __restrict__ tstart,
+                                                int64_t ntiles, int init, int64_t slot, int64_t nz_slots,
                                                 unsigned* __restrict__ tick) {
   if (v.sc[S::FROZEN] != 0.0) return;
   const double rho = v.sc[S::RHO];
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double rz = 0.0;
-  if (B < lv.n[k]) rz = down_node(lv, v, k, B, rho);
+  if (!tstart) {
+    const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (B < lv.n[k0]) rz = down_node(lv, v, k0, B, rho);
+  } else {
+    const int64_t j = blockIdx.x;
+    for (int t = k1 - k0; t >= 1; --t) {
+      const int32_t* ts = tstart + (int64_t)t * (ntiles + 1);
+      const int64_t e = ts[j + 1];
+      for (int64_t B = ts[j] + threadIdx.x; B < e; B += TPB) rz += down_node(lv, v, k0 + t - 1, B, rho);
+      __syncthreads();
+    }
+  }
   rz = block_sum<TPB>(rz);
   if (threadIdx.x == 0) v.zpart[slot + blockIdx.x] = rz;
-  if (k == 1 && last_cta(tick)) finish_rz(v, nz_slots, init);
+  if (k0 == 1 && last_cta(tick)) finish_rz(v, nz_slots, init);
 }
 
 // ------------------------------------------------------------ small kernels
@@ -705,6 +773,37 @@ T d2h(const T* d, cudaStream_t st) {
   MSP_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, st));
   MSP_CUDA(cudaStreamSynchronize(st));
   return v;
+}
+
+// the sweep steps of the expanded MSP below the coarse CTA: the solve
+// schedule's tile tiers (generic tiers level by
+// level), else one step per level up to pegp_Kc
+struct EStep {
+  int k0, k1;
+  const int32_t* tstart;
+  int64_t ntiles;
+  unsigned grid;
+};
+
+std::vector<EStep> e_steps(const Handle& h, int& Kc) {
+  std::vector<EStep> out;
+  const bool tiles = !h.tiers.empty() && std::getenv("MSP_PEGP_NOTILE") == nullptr;
+  int k = 1;
+  if (tiles) {
+    for (const auto& t : h.tiers) {
+      if (t.k0 != k) break;
+      if (t.generic || t.k1 - t.k0 < 1) {
+        for (int kk = t.k0; kk < t.k1; ++kk) out.push_back({kk, kk + 1, nullptr, 0, grid_for(h.lv[kk].n)});
+      } else {
+        out.push_back({t.k0, t.k1, t.tstart.p, t.ntiles, (unsigned)t.ntiles});
+      }
+      k = t.k1;
+    }
+  }
+  const int target = tiles ? std::max(k, h.Kc) : h.pegp_Kc;
+  for (; k < target; ++k) out.push_back({k, k + 1, nullptr, 0, grid_for(h.lv[k].n)});
+  Kc = k;
+  return out;
 }
 
 }  // namespace
@@ -882,9 +981,13 @@ void pegp_build(Handle& h, cudaStream_t st) {
   while (Kc < L - 1 && h.lv[Kc].n > CO_MAX) ++Kc;  // lv[Kc] is level Kc+1
   h.pegp_Kc = Kc;
   int64_t nup = 0, nz = 1;  // coarse CTA's (r, z) slot first
-  for (int k = 1; k < Kc; ++k) {
-    nup += grid_for(h.lv[k].n);
-    nz += grid_for(h.lv[k].n);
+  {
+    int kc = 1;
+    for (const auto& sp : e_steps(h, kc)) {
+      nup += sp.grid;
+      nz += sp.grid;
+    }
+    h.pegp_Kc = kc;
   }
   h.eup.alloc(3 * std::max<int64_t>(nup, 1));
   h.ezs.alloc(nz);
@@ -911,8 +1014,10 @@ HMat hmat(const Handle& h) {
   H.n0 = h.hclass[0];
   H.n1 = h.hclass[1];
   H.n2 = h.hclass[2];
-  H.b0 = (unsigned)((H.n0 + TPB / H_G0 - 1) / (TPB / H_G0));
-  H.b1 = (unsigned)((H.n1 + TPB / 32 - 1) / (TPB / 32));
+  // short and warp rows: persistent grid-stride CTAs (a few per SM), so the
+  // (p, q) ticket is taken by ~1k CTAs, not one per 32 rows
+  H.b0 = (unsigned)std::min<int64_t>((H.n0 + H_U * TPB / H_G0 - 1) / (H_U * TPB / H_G0), 148 * 3);
+  H.b1 = (unsigned)std::min<int64_t>((H.n1 + TPB / 32 - 1) / (TPB / 32), 148 * 2);
   H.b2 = (unsigned)h.hnseg;
   H.seg = h.hseg2.p;
   H.lnseg = h.hlnseg.p;
@@ -925,7 +1030,7 @@ HMat hmat(const Handle& h) {
 ELv elv(const Handle& h) {
   ELv lv{};
   lv.L = h.levels;
-  lv.Kc = h.pegp_Kc;
+  e_steps(h, lv.Kc);
   for (int k = 1; k <= h.levels; ++k) {
     lv.n[k - 1] = h.lv[k - 1].n;
     lv.off[k - 1] = h.lv[k - 1].off;
@@ -948,24 +1053,24 @@ void dot(Handle& h, int64_t n, const double* a, const double* b, double* out, cu
 // the preconditioner pass of one inner iteration (init: z0 = L_T~^+ r0 only)
 // on pair array zp (p read from .y, z written to .x)
 void e_sweeps(Handle& h, const ELv& lv, EVec v, int init, cudaStream_t st) {
-  const int Kc = lv.Kc;
+  int Kc = 1;
+  const std::vector<EStep> steps = e_steps(h, Kc);
   int64_t slot = 0;
-  for (int k = 1; k < Kc; ++k) {
-    const unsigned g = grid_for(lv.n[k]);
-    k_e_up<<<g, TPB, 0, st>>>(lv, v, k, init, slot);
-    slot += g;
+  for (const auto& sp : steps) {
+    k_e_up<<<sp.grid, TPB, 0, st>>>(lv, v, sp.k0, sp.k1, sp.tstart, sp.ntiles, init, slot);
+    slot += sp.grid;
   }
   const int64_t nup = slot;
   int64_t nz = 1;
-  for (int k = 1; k < Kc; ++k) nz += grid_for(lv.n[k]);
+  for (const auto& sp : steps) nz += sp.grid;
   k_e_coarse<<<1, CO_T, 0, st>>>(lv, v, init, nup, 0, nz);
   int64_t zs = nz;
-  for (int k = Kc - 1; k >= 1; --k) {
-    const unsigned g = grid_for(lv.n[k]);
-    zs -= g;
-    k_e_down<<<g, TPB, 0, st>>>(lv, v, k, init, zs, nz, h.etick.p + T_DOWN);
+  for (auto it = steps.rbegin(); it != steps.rend(); ++it) {
+    zs -= it->grid;
+    k_e_down<<<it->grid, TPB, 0, st>>>(lv, v, it->k0, it->k1, it->tstart, it->ntiles, init, zs, nz,
+                                       h.etick.p + T_DOWN);
   }
-  h.launches += 2 * (Kc - 1) + 1;
+  h.launches += 2 * (int64_t)steps.size() + 1;
 }
 
 EVec evec(Handle& h, double* x, int which) {
