@@ -395,6 +395,7 @@ def main():
         rep = solve(b, x)
         iters.append(rep["iterations"])
         launches += rep["kernel_launches"] + 1
+        last_rep = rep
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -512,7 +513,9 @@ def main():
             "scaling": "strong" if use_dist else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, g, extra, par),
-            "iterations": it, "time_to_rtol_s": ms_step / 1000.0, "setup_ms": info["setup_ms"],
+            "iterations": it, "converged": bool(last_rep["converged"]), "relres": float(last_rep["relres"]),
+            # not converged = the step is `maxit` outer iterations (a bounded sample of the solve)
+            "time_to_rtol_s": ms_step / 1000.0 if last_rep["converged"] else None, "setup_ms": info["setup_ms"],
             "solve_GBps_algorithmic": round(whole_gbps, 1) if whole_gbps else None,
             "roofline": roofline, "kernel_breakdown": breakdown,
             "cpu_baseline": cpu,

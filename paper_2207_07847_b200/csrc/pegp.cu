@@ -1016,8 +1016,11 @@ HMat hmat(const Handle& h) {
   H.n2 = h.hclass[2];
   // short and warp rows: persistent grid-stride CTAs (a few per SM), so the
   // (p, q) ticket is taken by ~1k CTAs, not one per 32 rows
-  H.b0 = (unsigned)std::min<int64_t>((H.n0 + H_U * TPB / H_G0 - 1) / (H_U * TPB / H_G0), 148 * 3);
-  H.b1 = (unsigned)std::min<int64_t>((H.n1 + TPB / 32 - 1) / (TPB / 32), 148 * 2);
+  // (MSP_PEGP_B0 / MSP_PEGP_B1: CTAs per SM of the two classes, for sweeps)
+  static const int per_sm0 = std::getenv("MSP_PEGP_B0") ? std::max(1, std::atoi(std::getenv("MSP_PEGP_B0"))) : 3;
+  static const int per_sm1 = std::getenv("MSP_PEGP_B1") ? std::max(1, std::atoi(std::getenv("MSP_PEGP_B1"))) : 2;
+  H.b0 = (unsigned)std::min<int64_t>((H.n0 + H_U * TPB / H_G0 - 1) / (H_U * TPB / H_G0), 148 * per_sm0);
+  H.b1 = (unsigned)std::min<int64_t>((H.n1 + TPB / 32 - 1) / (TPB / 32), 148 * per_sm1);
   H.b2 = (unsigned)h.hnseg;
   H.seg = h.hseg2.p;
   H.lnseg = h.hlnseg.p;
