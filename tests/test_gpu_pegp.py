@@ -151,3 +151,43 @@ def test_pcg_pegp(case):
     e -= e.mean()
     xs = ref.x - ref.x.mean()
     assert np.sqrt(abs(e @ (L @ e))) <= 1e-8 * np.sqrt(xs @ (L @ xs)), name
+
+
+def test_full_size_config1_pegp():
+    """configs[1] at full size (1,048,576 vertices, n~ = 1.94M, H~ with 37.9M
+    stored entries; the launch configuration `bench.py --precond pegp` times).
+    The oracle cannot factor L_H~ at this size in the suite's time, so the
+    apply is checked through what it can compute here:
+    * apply_LH on every row against the oracle's H~ edge weights in the
+      difference form, extended precision (1e-12);
+    * solve_LH (inner CG to 1e-13 + one double-double refinement step): its
+      true residual, formed with the ORACLE's assembled L_H~, is <= 2e-13
+      relative, and the solution has zero mean;
+    * apply_R PEGP = P(mu) solve_LH(P(mu)^T r) with the oracle's P on both
+      sides of the GPU inner solve (1e-12): the restriction / prolongation
+      wiring at this size."""
+    g = G.config_graph(1)
+    mu, seed = 0.8, 0
+    h = A.build_hierarchy(g, seed)
+    sysm = E.expand(g, h, mu)
+    s = M.setup(g.n, dt(g.rowptr, torch.int64), dt(g.col, torch.int32), dt(g.val), mu=mu, seed=seed)
+    assert s.pegp_info()["hnnz"] == sysm.WH.nnz
+    name = "config1_full_pegp"
+    x = np.random.default_rng(0).standard_normal(h.n_tilde)
+    y = s.apply_LH(dt(x)).cpu().numpy()
+    ref = np.asarray(PR._ld_laplacian_apply(sysm.WH.tocsr(), x), dtype=np.float64)
+    record(name, "apply_LH", float(np.abs(y - ref).max() / np.abs(ref).max()), 1e-12)
+    P = sysm.P
+    r = G.rhs(g.n, 8)
+    rt = P.T @ r
+    s.pegp_params(1e-13, 200000, 1)
+    zt, it = s.solve_LH(dt(rt))
+    zt = zt.cpu().numpy()
+    assert it > 0
+    rt0 = rt - rt.mean()
+    res = np.linalg.norm(sysm.LH @ zt - rt0)
+    record(name, "solve_LH_residual", float(res / np.linalg.norm(rt0)), 2e-13)
+    assert abs(zt.sum()) <= 1e-10 * np.abs(zt).sum()
+    z = s.apply_R(dt(r), precond="pegp").cpu().numpy()
+    zo = P @ zt
+    record(name, "apply_R_pegp_vs_P_solve_LH", float(np.abs(z - zo).max() / np.abs(zo).max()), 1e-12)
