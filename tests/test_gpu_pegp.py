@@ -177,7 +177,7 @@ def test_full_size_config1_pegp():
     y = s.apply_LH(dt(x)).cpu().numpy()
     ref = np.asarray(PR._ld_laplacian_apply(sysm.WH.tocsr(), x), dtype=np.float64)
     record(name, "apply_LH", float(np.abs(y - ref).max() / np.abs(ref).max()), 1e-12)
-    P = sysm.P
+    P = sysm.P()
     r = G.rhs(g.n, 8)
     rt = P.T @ r
     s.pegp_params(1e-13, 200000, 1)
