@@ -449,8 +449,9 @@ def main():
     kt = int(info["tile_level"])
     n_own = g.n if not use_dist else int(drange[1] - drange[0])
     nnz_own = g.nnz_adj if not use_dist else int(round(g.nnz_adj * n_own / g.n))
-    model = {"spmv": spmv_bytes(n_own, nnz_own), "tile_up": tile_up_bytes(sz, kt)}
-    if kt >= 2:
+    model = {"spmv": spmv_bytes(n_own, nnz_own)}
+    if kt >= 2:  # a generic (per-level) first tier has no tile byte model: its sweeps report time only
+        model["tile_up"] = tile_up_bytes(sz, kt)
         model["tile_down"] = tile_down_bytes(sz, kt)
     if use_dist and world > 1:  # the tile byte models are whole-graph figures
         model = {"spmv": model["spmv"]}
