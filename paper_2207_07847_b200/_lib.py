@@ -57,6 +57,15 @@ def _load():
     if not os.path.exists(_LIBPATH):
         raise ImportError(f"{_LIBPATH} is not built: run `python -m paper_2207_07847_b200.build` "
                           "(there is no CPU fallback)")
+    # libmsp_b200.so needs libnccl.so.2.  torch bundles the NCCL build it was
+    # linked against; if the system's (older) copy were loaded first through
+    # our dependency, a later `import torch` in the same process would bind to
+    # it and fail on missing symbols.  Loading torch first makes both use
+    # torch's copy (same soname).
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     L = ctypes.CDLL(_LIBPATH)
     P, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.msp_setup.argtypes = [i64, P, P, P, ctypes.c_int, ctypes.POINTER(_Params), P, ctypes.POINTER(P)]

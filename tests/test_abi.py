@@ -66,3 +66,16 @@ def test_product_path_does_not_import_oracle():
         if f.endswith((".py", ".cu", ".cuh", ".h")):
             s = open(f).read()
             assert "oracle" not in re.sub(r"#.*|//.*", "", s).replace("no oracle", ""), f
+
+
+def test_library_load_then_torch_import():
+    """build() followed by smoke() in one process: loading the native library
+    (which depends on libnccl.so.2) before `import torch` must not bind torch
+    to an older system NCCL -- the binding loads torch's copy first."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import paper_2207_07847_b200 as M; M.load(); import torch; "
+            "import torch.distributed; print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
