@@ -528,6 +528,7 @@ void pcg_dist_group(std::vector<Handle*>& hs, bool loop, double rtol, int maxit,
   if (const char* e = std::getenv("MSP_PCG_BATCH")) batch = std::max(2, std::atoi(e) & ~1);
   const bool use_graph = std::getenv("MSP_NO_GRAPH") == nullptr && !hs[0]->profile;
   cudaGraphExec_t gx = nullptr;
+  int64_t graph_launches = 0;  // kernels of one captured batch (counted on rank 0's handle)
   unsigned hc[C_NCNT];
   auto done = [&]() {
     MSP_CUDA(cudaMemcpyAsync(hc, hs[0]->counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -545,12 +546,16 @@ void pcg_dist_group(std::vector<Handle*>& hs, bool loop, double rtol, int maxit,
           cudaGraph_t gr;
           DistGroup gc = g;
           gc.st = cs;
+          const int64_t lc0 = hs[0]->launches;
           MSP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
           for (int b2 = 0; b2 < nb; ++b2) dist_iteration(gc, P.data());
           MSP_CUDA(cudaStreamEndCapture(cs, &gr));
           MSP_CUDA(cudaGraphInstantiate(&gx, gr, 0));
           cudaGraphDestroy(gr);
           cudaStreamDestroy(cs);
+          graph_launches = hs[0]->launches - lc0;  // the capture pass counted the first replay
+        } else {
+          hs[0]->launches += graph_launches;
         }
         MSP_CUDA(cudaGraphLaunch(gx, st));
       } else {
